@@ -1,0 +1,389 @@
+#!/usr/bin/env python3
+"""bench.py -- Force2Vec minibatch-SGD epochs on B200 (BASELINE.json metric:
+edge+neg-sample updates/s and sec/epoch at d=128; % of HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c2|c1|c3|c4]
+
+A "step" is one epoch of train() (trainer.cpp:211-249) over the whole graph:
+every batch's fused gradient + update.  Default workload = BASELINE config 2
+(R-MAT scale 20, edge factor 16, (.57,.19,.19,.05), symmetrised/deduplicated,
+t-distribution, d=128, b=384, s=5, lr=.02, 5-epoch schedule, Philox
+negatives, Z ~ U(-1,1)), synthetic (no dataset).
+
+Printed JSON (rank 0, one line):
+  value  = (nnz + n*s) * K / (device time of K epochs), inputs resident in HBM,
+           timed with CUDA events on the library's stream;
+  e2e    = same metric through the public API with host buffers: per step one
+           full train() of the config (5 epochs) including H2D of CSR + Z from
+           pinned memory and D2H of Z;
+  roofline = algorithmic bytes per epoch-kernel launch / its event-timed
+           duration vs MEASURED_PEAKS.json hbm_gbs; traffic from the committed
+           ncu capture (profiles/) when it matches the config;
+  cpu_baseline = the unmodified reference (oracle/_ref) on this host's cores
+           over a bounded sample of batches.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+CONFIGS = {
+    # name: (generator, kwargs, kind, d, b, s, lr, epochs)
+    "c1": ("sbm", dict(n=4096, blocks=8, p_in=0.03, p_out=0.001, seed=4096), "sigmoid", 128, 256,
+           5, 0.02, 10),
+    "c2": ("rmat", dict(scale=20, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1), "tdist", 128,
+           384, 5, 0.02, 5),
+    "c3": ("chung_lu", dict(n=3_000_000, exponent=2.2, min_deg=2.0, max_deg=30000.0,
+                            mean_deg=78.0, seed=1), "sigmoid", 128, 384, 5, 0.02, 1),
+    "c4": ("rgg", dict(n=1_000_000, mean_deg=12.0, seed=1), "tdist", 2, 256, 5, 0.02, 20),
+}
+WORKLOAD_NAMES = {
+    "c1": "SBM n=4096 (8 blocks, p_in .03, p_out .001), sigmoid, d=128, b=256, s=5, lr .02",
+    "c2": "R-MAT scale 20 (ef 16, .57/.19/.19/.05), t-dist, d=128, b=384, s=5, lr .02",
+    "c3": "Chung-Lu n=3M power-law 2.2 (min 2, max 30000, mean 78), sigmoid, d=128, b=384, s=5",
+    "c4": "RGG n=1M unit square (mean degree 12), t-dist, d=2, b=256, s=5, lr .02",
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def make_graph(f2v, cfg_name):
+    gen, kw, *_ = CONFIGS[cfg_name]
+    t0 = time.perf_counter()
+    if gen == "sbm":
+        g = f2v.sbm_graph(kw["n"], kw["blocks"], kw["p_in"], kw["p_out"], kw["seed"])
+    elif gen == "rmat":
+        g = f2v.rmat_graph(kw["scale"], kw["edge_factor"], kw["a"], kw["b"], kw["c"], kw["seed"])
+    elif gen == "chung_lu":
+        g = f2v.chung_lu_graph(kw["n"], kw["exponent"], kw["min_deg"], kw["max_deg"],
+                               kw["mean_deg"], kw["seed"])
+    else:
+        g = f2v.rgg_graph(kw["n"], kw["mean_deg"], kw["seed"])
+    log(f"graph {cfg_name}: n={g.num_vertices()} nnz={g.num_edges()} "
+        f"max_deg={int(g.degrees().max())} built in {time.perf_counter() - t0:.1f}s")
+    return g
+
+
+def algorithmic_bytes(n, nnz, d, b, s):
+    """nnz(4d+4) + n(8d+20) + ceil(n/b) s (4d+4) bytes per epoch."""
+    return nnz * (4 * d + 4) + n * (8 * d + 20) + ((n + b - 1) // b) * s * (4 * d + 4)
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                      f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.1)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def ncu_traffic(cfg_name):
+    """dram bytes per epoch-kernel launch from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            t = json.load(f)
+        e = t.get(cfg_name)
+        return e["dram_bytes_per_launch"] if e else None
+    except Exception:
+        return None
+
+
+def reference_cpu(g, z0, cfg_name, budget_s=20.0, workers=None, sample_batches=None):
+    """The unmodified reference core (oracle/_ref) on this host's cores, over a
+    bounded prefix of epoch 0's batches: partition_epoch + build_minibatch +
+    make_schedule + grad_minibatch + apply_update (trainer.cpp:210-236)."""
+    import ctypes as C
+    import pyoracle as P
+
+    _, _, kind, d, b, s, lr, _ = CONFIGS[cfg_name]
+    kind_id = P.KINDS[kind]
+    n = g.num_vertices()
+    workers = workers or os.cpu_count()
+    kindname = "reference"
+    if P.reference_available():
+        R = P.reference()
+        t0 = time.perf_counter()
+        rg = P.RefGraph.from_csr(g.row_offsets, g.col_indices)
+        log(f"reference CsrGraph::from_edges: {time.perf_counter() - t0:.1f}s")
+
+        def run(nb):
+            pairs = C.c_uint64()
+            z = np.array(z0, copy=True)
+            secs = R.ref_time_batches(rg.ptr, z, d, b, s, np.float32(lr), kind_id, 1, workers, nb,
+                                      C.byref(pairs))
+            return secs, pairs.value
+    else:  # the C restatement (single-threaded port per batch, pthreads per batch)
+        kindname = "port"
+        O = P.oracle()
+        perm = P.orc_epoch_perm(n, min(b, n), 1, 0)
+
+        def run(nb):
+            z = np.array(z0, copy=True)
+            t0 = time.perf_counter()
+            pairs = 0
+            for bi in range(nb):
+                ids = perm[bi * b:(bi + 1) * b]
+                negs = P.orc_negatives("philox", 1, 0, bi, n, s)
+                rc, grads, _ = P.orc_grad_minibatch(g.row_offsets, g.col_indices, z, ids, negs,
+                                                    kind, threads=workers)
+                O.orc_apply_update(z, d, ids, len(ids), grads, np.float32(lr))
+                pairs += int((g.row_offsets[ids + 1] - g.row_offsets[ids]).sum()) + len(ids) * s
+            return time.perf_counter() - t0, pairs
+    nb_total = (n + b - 1) // b
+    if sample_batches is None:
+        probe = min(nb_total, 16)
+        secs, _ = run(probe)
+        sample_batches = int(min(nb_total, max(probe, probe * budget_s / max(secs, 1e-6))))
+    secs, pairs = run(sample_batches)
+    return {"value": pairs / secs, "unit": "updates/s", "cores": workers, "kind": kindname,
+            "sample": f"first {sample_batches} of {nb_total} batches of epoch 0 "
+                      f"({pairs} pair updates, {secs:.1f}s, {workers} worker threads)",
+            "sec_per_epoch_extrapolated": secs * nb_total / sample_batches}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def bench_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import paper_2009_10035_b200 as f2v
+
+    cfg_name = args.config
+    _, _, kind, d, b, s, lr, epochs = CONFIGS[cfg_name]
+    g = make_graph(f2v, cfg_name)
+    n = g.num_vertices()
+    import pyoracle as P
+    z0 = np.zeros((n, d), np.float32)
+    P.oracle().orc_random_embedding(n, d, 1, z0)
+    # per step: a bounded sample of the same workload (budget split over steps)
+    per_step = max(3.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
+    first = reference_cpu(g, z0, cfg_name, budget_s=per_step)
+    nb = int(first["sample"].split()[1])
+    vals = [first["value"]]
+    for _ in range(max(0, args.steps - 1)):
+        vals.append(reference_cpu(g, z0, cfg_name, sample_batches=nb)["value"])
+    v = float(np.median(vals))
+    nnz = g.num_edges()
+    out = {
+        "impl": "reference", "metric": "edge+neg-sample updates/sec (d=128)" if d == 128 else
+        "edge+neg-sample updates/sec", "value": v, "unit": "updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * (nnz + n * s) / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD_NAMES[cfg_name], "n": n, "nnz": nnz, "batch": b,
+                   "negatives": s, "epoch_sample": first["sample"]},
+        "sec_per_epoch": (nnz + n * s) / v,
+        "cpu_baseline": {k: first[k] for k in ("cores", "kind", "sample")} | {"value": v,
+                                                                             "unit": "updates/s"},
+        "e2e": {"value": v, "unit": "updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def bench_b200(args):
+    import paper_2009_10035_b200 as f2v
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    cfg_name = args.config
+    _, _, kind, d, b, s, lr, epochs = CONFIGS[cfg_name]
+    g = make_graph(f2v, cfg_name)
+    n, nnz = g.num_vertices(), g.num_edges()
+    # epochs schedule long enough that warm-up and timed epochs each get their
+    # own epoch index (own Fisher-Yates perm and negatives); lr is constant.
+    cfg = f2v.TrainConfig(dim=d, batch=b, negatives=s, lr=lr,
+                          epochs=args.warmup + args.steps,
+                          model=f2v.ForceModel(f2v.ForceKind.parse(kind)), seed=1,
+                          monitor_loss=False, sampler="philox")
+    dev = f2v.Device(local)
+    dev.upload_graph(g)
+    dev.uniform_embedding(n, d, 1, -1.0, 1.0)  # the configs' U(-1,1) from Rng(seed, 0)
+    dev.train_epochs(cfg, 0, args.warmup)  # untimed warm-up epochs
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    f2v._lib.f2v_kernel_launches(dev._h, 1)
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        dev.train_epochs(cfg, args.warmup, args.steps)  # K timed epochs, one call
+        t_wall = time.perf_counter() - t_wall
+    t = dev.last_timing()
+    dev_ms, kern_ms, nk = t["device_ms"], t["epoch_kernel_ms"], t["epoch_kernels"]
+    assert nk == args.steps
+    launches = f2v._lib.f2v_kernel_launches(dev._h, 0)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        tt = torch.tensor([dev_ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_ms = float(tt.item())
+    z = dev.get_embedding()
+    assert np.all(np.isfinite(z)), "non-finite embedding"
+    pairs = nnz + n * s
+    value = world * pairs * args.steps / (dev_ms / 1e3)
+    ms_per_step = dev_ms / args.steps
+    algo = algorithmic_bytes(n, nnz, d, min(b, n), s)
+    peak, peak_kind = hbm_peak()
+    achieved = algo / (kern_ms / nk / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": ncu_traffic(cfg_name),
+            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
+            else "fallback 6650 GB/s (B200_PROFILING.md)",
+            "algorithmic_bytes_per_launch": algo,
+            "kernel_ms_per_launch": kern_ms / nk}
+    # ------------------------------------------------------------ e2e
+    import torch
+    h_row = torch.from_numpy(g.row_offsets).pin_memory().numpy()
+    h_col = torch.from_numpy(g.col_indices).pin_memory().numpy()
+    h_z0 = torch.empty((n, d), dtype=torch.float32).pin_memory().numpy()
+    h_z = torch.empty((n, d), dtype=torch.float32).pin_memory().numpy()
+    dev.uniform_embedding(n, d, 1, -1.0, 1.0)
+    h_z0[:] = dev.get_embedding()
+    e2e_steps = max(1, min(args.steps, 3))
+    g_pinned = f2v.CsrGraph(h_row, h_col)
+
+    cfg_e2e = f2v.TrainConfig(dim=d, batch=b, negatives=s, lr=lr, epochs=epochs,
+                              model=cfg.model, seed=1, monitor_loss=False, sampler="philox")
+
+    def e2e_once():
+        dev.upload_graph(g_pinned)
+        dev.set_embedding(h_z0)
+        dev.train_epochs(cfg_e2e, 0, 0)
+        out = np.ascontiguousarray(h_z)
+        f2v._lib.f2v_get_embedding(dev._h, out)
+        return out
+    e2e_once()  # warm
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_once()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e_val = world * pairs * epochs / e2e_s
+    h2d = h_row.nbytes + h_col.nbytes + h_z0.nbytes + 4 * n * epochs  # + perms
+    d2h = h_z.nbytes
+    dev.close()
+    if rank != 0:
+        return 0
+    out = {
+        "metric": "edge+neg-sample updates/sec (d=128)" if d == 128 else
+        "edge+neg-sample updates/sec", "value": value, "unit": "updates/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD_NAMES[cfg_name], "n": n, "nnz": nnz, "batch": b,
+                   "negatives": s, "epochs_schedule": epochs, "sampler": "philox",
+                   "step": "one epoch (all batches) of train()",
+                   "l2": "inputs larger than L2 (Z 2x%d MB + CSR %d MB > 126 MB)" %
+                         (n * d * 4 >> 20, (nnz * 4 + n * 8) >> 20)},
+        "sec_per_epoch": ms_per_step / 1e3,
+        "roofline": roof,
+        "e2e": {"value": e2e_val, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h),
+                "step": f"one train() of the {epochs}-epoch schedule via the public API "
+                        f"(host CSR+Z in from pinned memory, Z out): {e2e_s * 1e3:.1f} ms"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "wall_s_timed_region": t_wall,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        z0 = h_z0
+        try:
+            out["cpu_baseline"] = reference_cpu(g, z0, cfg_name, budget_s=args.cpu_budget)
+        except Exception as ex:  # reported, not hidden
+            out["cpu_baseline"] = {"value": None, "error": str(ex)}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        log("note: warm-up raised to the contract minimum of 3")
+        args.warmup = 3
+    if args.impl == "reference":
+        return bench_reference(args)
+    return bench_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,185 @@
+/* include/force2vec_b200.h -- the drop-in C-ABI for Force2Vec's minibatch SGD
+ * step on B200 (sm_100a).  Plain C: <stdint.h> types, pointers and sizes; no
+ * C++ or torch types cross this boundary.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/proj/core/...).  Return codes mirror the reference's
+ * exception taxonomy (errors.hpp:8-40, CLI mapping force2vec.cpp:23-26):
+ *   F2V_OK 0, F2V_EUSAGE 1 (UsageError), F2V_EIO 2 (IoError),
+ *   F2V_ERANGE 3 (FormatError/RangeError), F2V_ENUMERICAL 4 (NumericalError),
+ *   F2V_ECUDA 5 (device/driver failure), F2V_EUNSUPPORTED 6 (UnsupportedError).
+ * f2v_last_error() returns the message the reference would have thrown, e.g.
+ * "non-finite gradient for vertex 7 (epoch 0, batch 3)" (trainer.cpp:149-152,
+ * 229-233).
+ *
+ * Threading: one context per training run, not thread-safe per context; every
+ * call is synchronous (work runs on the context's own CUDA stream).  There is
+ * no CPU fallback: f2v_create fails with F2V_ECUDA when no sm_100 device is
+ * present.
+ */
+#ifndef FORCE2VEC_B200_H
+#define FORCE2VEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define F2V_OK 0
+#define F2V_EUSAGE 1
+#define F2V_EIO 2
+#define F2V_ERANGE 3
+#define F2V_ENUMERICAL 4
+#define F2V_ECUDA 5
+#define F2V_EUNSUPPORTED 6
+
+/* ForceKind, force_kernels.hpp:12 (same order) */
+#define F2V_SIGMOID 0
+#define F2V_TDIST 1
+#define F2V_FR 2
+#define F2V_FA 3
+#define F2V_LINLOG 4
+
+/* negative-sample streams */
+#define F2V_SAMPLER_SPLITMIX 0 /* the reference's Rng::keyed(seed,{0x33,epoch,batch}) */
+#define F2V_SAMPLER_PHILOX 1   /* Philox4x32-10 keyed by seed, counter (k,batch,epoch,shard) */
+
+/* ForceModel, force_kernels.hpp:17-21 */
+typedef struct {
+  int32_t kind;          /* F2V_SIGMOID .. F2V_LINLOG */
+  float epsilon;         /* singularity clamp, default 1e-6f */
+  float repulsion_cap;   /* <= 0: std::nullopt (no clamp); default 5.0f */
+} f2v_force_model;
+
+/* TrainConfig, trainer.hpp:15-30 (+ the device-side fields of SURVEY §8b) */
+typedef struct {
+  uint32_t dim;          /* d */
+  uint32_t batch;        /* b, clamped to n as train() does (trainer.cpp:200) */
+  uint32_t negatives;    /* s, shared per batch (sampling.cpp:59) */
+  float lr;
+  uint32_t epochs;
+  f2v_force_model model;
+  uint64_t seed;
+  int32_t lr_decay;      /* 0 Constant, 1 LinearToZero (trainer.cpp:212-214) */
+  int32_t monitor_loss;  /* 1: per-epoch loss on the pre-update snapshot */
+  int32_t sampler;       /* F2V_SAMPLER_* */
+  int32_t init;          /* 0: caller's Z; 1: init_embedding (trainer.cpp:62-72) */
+  uint32_t first_epoch;  /* run epochs [first_epoch, first_epoch + run_epochs) of the */
+  uint32_t run_epochs;   /* `epochs`-long schedule; run_epochs 0 = through the end */
+} f2v_train_config;
+
+/* TrainCounters, trainer.hpp:83-87 */
+typedef struct {
+  uint64_t attractive_evals;
+  uint64_t repulsive_evals;
+} f2v_counters;
+
+/* where a NumericalError happened */
+typedef struct {
+  uint32_t epoch;
+  uint64_t batch;
+  uint32_t vertex;
+} f2v_failure;
+
+typedef struct f2v_ctx f2v_ctx;
+
+/* ------------------------------------------------------------ context */
+/* device = CUDA ordinal. Returns NULL on failure (see f2v_global_error()). */
+f2v_ctx* f2v_create(int32_t device);
+void f2v_destroy(f2v_ctx* ctx);
+const char* f2v_last_error(const f2v_ctx* ctx);
+const char* f2v_global_error(void);
+/* kernels launched by this context since the last reset (bench evidence) */
+uint64_t f2v_kernel_launches(const f2v_ctx* ctx, int32_t reset);
+/* CUDA-event timing of the last f2v_train_epochs call, on the context's
+ * stream: out[0] device ms of the whole call, out[1] summed ms of the
+ * persistent epoch kernels, out[2] number of epoch kernels, out[3] host
+ * wall ms of the call. */
+int32_t f2v_last_timing(const f2v_ctx* ctx, double* out4);
+
+/* ---------------------------------------------- graph + embedding state */
+/* CsrGraph (csr_graph.hpp:24-101): row_offsets u64[n+1], col_indices u32[nnz];
+ * must be canonical (sorted, unique rows) -- use f2v_csr_from_edges. */
+int32_t f2v_upload_graph(f2v_ctx* ctx, uint32_t n, const uint64_t* row_offsets,
+                         const uint32_t* col_indices, uint64_t nnz);
+/* EmbeddingMatrix (trainer.hpp:33-57): row-major f32[n*d] */
+int32_t f2v_set_embedding(f2v_ctx* ctx, const float* z, uint32_t n, uint32_t d);
+int32_t f2v_get_embedding(f2v_ctx* ctx, float* z);
+/* init_embedding (trainer.cpp:62-72): U(-0.5/d, 0.5/d) keyed (seed,{0x11}) */
+int32_t f2v_init_embedding(f2v_ctx* ctx, uint32_t n, uint32_t d, uint64_t seed);
+/* the configs' U(lo,hi) from Rng(seed,0) (test_trainer.cpp:18-23), on device */
+int32_t f2v_uniform_embedding(f2v_ctx* ctx, uint32_t n, uint32_t d, uint64_t seed, float lo,
+                              float hi);
+
+/* --------------------------------- per-step operators (the reference seam) */
+/* grad_minibatch (trainer.hpp:93-96, trainer.cpp:108-165) over the one-hop
+ * minibatch {ids, negatives} against the device Z.  grads_out (nullable) is a
+ * host f32[b*d]; the gradient also stays staged on the device for
+ * f2v_apply_update(grads = NULL).  On a non-finite gradient returns
+ * F2V_ENUMERICAL with *bad_vertex = first such vertex in batch order. */
+int32_t f2v_grad_minibatch(f2v_ctx* ctx, const uint32_t* ids, uint32_t b,
+                           const uint32_t* negatives, uint32_t s, f2v_force_model model,
+                           float* grads_out, f2v_counters* counters, uint32_t* bad_vertex);
+/* apply_update (trainer.hpp:99-100): z[ids[i]] -= eta * grads[i];
+ * grads NULL = the staged gradient of the last f2v_grad_minibatch. */
+int32_t f2v_apply_update(f2v_ctx* ctx, const uint32_t* ids, uint32_t b, const float* grads,
+                         float eta);
+/* batch_loss (trainer.hpp:103-104) on the device Z */
+int32_t f2v_batch_loss(f2v_ctx* ctx, const uint32_t* ids, uint32_t b, const uint32_t* negatives,
+                       uint32_t s, f2v_force_model model, double* loss_out);
+/* fused grad (+loss) + apply of one batch; Z untouched when F2V_ENUMERICAL */
+int32_t f2v_step(f2v_ctx* ctx, const uint32_t* ids, uint32_t b, const uint32_t* negatives,
+                 uint32_t s, f2v_force_model model, float eta, double* loss_out,
+                 f2v_counters* counters, uint32_t* bad_vertex);
+
+/* ------------------------------------------------- device-resident epochs */
+/* The train() epoch loop (trainer.cpp:211-249) on device: per epoch the
+ * Fisher-Yates partition_epoch (sampling.cpp:7-19), the negatives, every
+ * batch's grad_minibatch + batch_loss + apply_update in one persistent
+ * dataflow kernel.  epoch_loss_out (nullable) gets one double per epoch run when
+ * monitor_loss.  On F2V_ENUMERICAL, Z holds the state after the last
+ * complete batch and *failure says where. */
+int32_t f2v_train_epochs(f2v_ctx* ctx, const f2v_train_config* cfg, double* epoch_loss_out,
+                         f2v_counters* counters, f2v_failure* failure);
+
+/* train(g, cfg) (trainer.hpp:115-116) with host buffers: uploads the CSR and
+ * z_inout (or initialises it, cfg->init), runs cfg->epochs epochs, copies Z
+ * back.  device = CUDA ordinal. */
+int32_t f2v_train(int32_t device, uint32_t n, const uint64_t* row_offsets,
+                  const uint32_t* col_indices, uint64_t nnz, float* z_inout,
+                  const f2v_train_config* cfg, double* epoch_loss_out, f2v_counters* counters,
+                  f2v_failure* failure);
+
+/* ------------------------------------------- host-side data formats (C++) */
+/* CsrGraph::from_edges (csr_graph.cpp:57-97), parallel, byte-identical.
+ * pairs = u32[2*m]; col_out capacity >= (symmetrize ? 2m : m).
+ * Returns F2V_ERANGE on an out-of-range endpoint. */
+int32_t f2v_csr_from_edges(const uint32_t* pairs, uint64_t m, uint32_t n, int32_t symmetrize,
+                           uint64_t* row_offsets_out, uint32_t* col_out, uint64_t* nnz_out,
+                           uint64_t* duplicates_dropped, uint64_t* self_loops_dropped);
+/* partition_epoch (sampling.cpp:7-19) for train()'s key (seed,{0x22,epoch}) */
+int32_t f2v_partition_epoch(uint32_t n, uint32_t b, uint64_t seed, uint32_t epoch,
+                            uint32_t* perm_out);
+/* the negatives of (epoch, batch[, shard]) under a sampler, host side */
+int32_t f2v_negatives(int32_t sampler, uint64_t seed, uint32_t epoch, uint64_t batch,
+                      uint32_t shard, uint32_t num_shards, uint32_t n, uint32_t s,
+                      uint32_t* out);
+
+/* Synthetic graph generators (BASELINE configs).  Each returns an arc list
+ * (u32[2*m], caller frees with f2v_free) for f2v_csr_from_edges. */
+int32_t f2v_gen_sbm(uint32_t n, int32_t blocks, double p_in, double p_out, uint64_t seed,
+                    uint32_t** pairs_out, uint64_t* m_out);
+int32_t f2v_gen_rmat(uint32_t scale, uint32_t edge_factor, double a, double b, double c,
+                     uint64_t seed, uint32_t** pairs_out, uint64_t* m_out);
+int32_t f2v_gen_chung_lu(uint32_t n, double exponent, double min_deg, double max_deg,
+                         double mean_deg, uint64_t seed, uint32_t** pairs_out, uint64_t* m_out);
+int32_t f2v_gen_rgg(uint32_t n, double mean_deg, uint64_t seed, uint32_t** pairs_out,
+                    uint64_t* m_out);
+void f2v_free(void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FORCE2VEC_B200_H */

@@ -1,0 +1,572 @@
+// f2v_capi.cpp -- the extern "C" boundary (include/force2vec_b200.h) and the
+// host-side training driver above the device kernels.  Mirrors the reference
+// API: train() (trainer.cpp:192-251), grad_minibatch / apply_update /
+// batch_loss (trainer.hpp:93-104), error taxonomy (errors.hpp:8-40).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <future>
+#include <string>
+#include <vector>
+
+#include "f2v_internal.h"
+#include "f2v_rng.h"
+
+namespace f2v {
+
+void csr_from_edges(const uint32_t* pairs, uint64_t m, uint32_t n, bool symmetrize,
+                    uint64_t* rowptr, uint32_t* col_out, uint64_t* nnz_out, uint64_t* dups_out,
+                    uint64_t* loops_out);
+void partition_epoch(uint32_t n, uint32_t b, uint64_t state, uint32_t* perm);
+std::vector<uint32_t> gen_sbm(uint32_t n, int blocks, double p_in, double p_out, uint64_t seed);
+std::vector<uint32_t> gen_rmat(uint32_t scale, uint32_t ef, double a, double b, double c,
+                               uint64_t seed);
+std::vector<uint32_t> gen_chung_lu(uint32_t n, double expo, double min_deg, double max_deg,
+                                   double mean_deg, uint64_t seed);
+std::vector<uint32_t> gen_rgg(uint32_t n, double mean_deg, uint64_t seed);
+
+void fail(int32_t code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(F2V_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what);
+}
+
+void DeviceBuf::ensure(size_t want) {
+  if (want <= bytes && p) return;
+  release();
+  F2V_CUDA(cudaMalloc(&p, std::max<size_t>(want, 16)));
+  bytes = std::max<size_t>(want, 16);
+}
+
+void DeviceBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+static thread_local std::string g_global_err;
+
+static int32_t guard(Ctx* c, const std::function<void()>& fn) {
+  try {
+    fn();
+    if (c) c->err.clear();
+    return F2V_OK;
+  } catch (const Error& e) {
+    if (c) c->err = e.msg;
+    g_global_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (c) c->err = "host out of memory";
+    g_global_err = "host out of memory";
+    return F2V_ECUDA;
+  } catch (const std::exception& e) {
+    if (c) c->err = e.what();
+    g_global_err = e.what();
+    return F2V_ECUDA;
+  }
+}
+
+static void need_graph(const Ctx& c) {
+  if (!c.rowptr.p) fail(F2V_EUSAGE, "no graph uploaded");
+}
+static void need_embedding(const Ctx& c) {
+  if (!c.z[c.cur].p || c.d == 0) fail(F2V_EUSAGE, "no embedding set");
+}
+
+static void validate_model(const f2v_force_model& m) {
+  if (m.kind < F2V_SIGMOID || m.kind > F2V_LINLOG) fail(F2V_EUSAGE, "unknown force model");
+}
+
+// Stage ids/negatives of one minibatch on the device (RangeError like
+// CsrGraph::neighbors, csr_graph.hpp:40-43).
+static bool stage_batch(Ctx& c, const uint32_t* ids, uint32_t b, const uint32_t* negs,
+                        uint32_t s) {
+  for (uint32_t i = 0; i < b; ++i)
+    if (ids[i] >= c.n) fail(F2V_ERANGE, "vertex id out of range");
+  for (uint32_t k = 0; k < s; ++k)
+    if (negs[k] >= c.n) fail(F2V_ERANGE, "vertex id out of range");
+  c.ids.ensure(sizeof(uint32_t) * std::max<uint32_t>(b, 1));
+  c.negs.ensure(sizeof(uint32_t) * std::max<uint32_t>(s, 1));
+  c.grads.ensure(sizeof(float) * std::max<size_t>(size_t(b) * c.d, 1));
+  c.vloss.ensure(sizeof(double) * std::max<uint32_t>(b, 1));
+  c.bad.ensure(sizeof(unsigned long long));
+  if (b)
+    F2V_CUDA(cudaMemcpyAsync(c.ids.p, ids, sizeof(uint32_t) * b, cudaMemcpyHostToDevice,
+                             c.stream));
+  if (s)
+    F2V_CUDA(cudaMemcpyAsync(c.negs.p, negs, sizeof(uint32_t) * s, cudaMemcpyHostToDevice,
+                             c.stream));
+  std::vector<uint32_t> sorted(ids, ids + b);
+  std::sort(sorted.begin(), sorted.end());
+  return std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+}
+
+static uint64_t read_bad(Ctx& c) {
+  uint64_t bad = 0;
+  F2V_CUDA(cudaMemcpyAsync(&bad, c.bad.p, sizeof(bad), cudaMemcpyDeviceToHost, c.stream));
+  F2V_CUDA(cudaStreamSynchronize(c.stream));
+  return bad;
+}
+
+static uint64_t degree_sum(const Ctx& c, const uint32_t* ids, uint32_t b) {
+  uint64_t s = 0;
+  for (uint32_t i = 0; i < b; ++i) s += c.h_rowptr[ids[i] + 1] - c.h_rowptr[ids[i]];
+  return s;
+}
+
+// -------------------------------------------------------- train() driver
+// trainer.cpp:192-251 on the device.  Per epoch: eta (212-214), the
+// Fisher-Yates partition (216-217, computed on the host one epoch ahead while
+// the GPU runs), then one dataflow launch covering every batch's
+// grad_minibatch + batch_loss + apply_update (220-236).
+static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_out,
+                              f2v_counters* counters, f2v_failure* failure);
+
+// Timing wrapper: CUDA events on the context stream around the whole call.
+static void train_epochs(Ctx& c, const f2v_train_config& cfg, double* loss_out,
+                         f2v_counters* counters, f2v_failure* failure) {
+  if (!c.ev_begin) {
+    F2V_CUDA(cudaEventCreate(&c.ev_begin));
+    F2V_CUDA(cudaEventCreate(&c.ev_end));
+  }
+  for (double& t : c.timing) t = 0.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  F2V_CUDA(cudaEventRecord(c.ev_begin, c.stream));
+  train_epochs_impl(c, cfg, loss_out, counters, failure);
+  F2V_CUDA(cudaEventRecord(c.ev_end, c.stream));
+  F2V_CUDA(cudaEventSynchronize(c.ev_end));
+  float ms = 0.f;
+  F2V_CUDA(cudaEventElapsedTime(&ms, c.ev_begin, c.ev_end));
+  c.timing[0] = ms;
+  c.timing[3] =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+}
+
+static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_out,
+                              f2v_counters* counters, f2v_failure* failure) {
+  need_graph(c);
+  if (cfg.dim < 1) fail(F2V_EUSAGE, "dim must be >= 1");  // trainer.cpp:13-22
+  if (cfg.batch < 1) fail(F2V_EUSAGE, "batch must be >= 1");
+  if (cfg.negatives < 1) fail(F2V_EUSAGE, "negatives must be >= 1");
+  if (!(cfg.lr > 0)) fail(F2V_EUSAGE, "lr must be > 0");
+  if (cfg.epochs < 1) fail(F2V_EUSAGE, "epochs must be >= 1");
+  if (cfg.first_epoch >= cfg.epochs) fail(F2V_EUSAGE, "first_epoch must be < epochs");
+  const uint32_t end_epoch =
+      cfg.run_epochs ? std::min(cfg.epochs, cfg.first_epoch + cfg.run_epochs) : cfg.epochs;
+  validate_model(cfg.model);
+  if (cfg.monitor_loss && cfg.model.kind != F2V_SIGMOID && cfg.model.kind != F2V_TDIST)
+    fail(F2V_EUNSUPPORTED, "loss monitoring requires the sigmoid or tdist model");
+  if (cfg.sampler != F2V_SAMPLER_SPLITMIX && cfg.sampler != F2V_SAMPLER_PHILOX)
+    fail(F2V_EUSAGE, "unknown sampler");
+  if (c.n >= 0x80000000u) fail(F2V_EUSAGE, "n must be < 2^31");
+  if (cfg.init == 1) {
+    c.d = cfg.dim;
+    c.cur = 0;
+    c.z[0].ensure(sizeof(float) * size_t(c.n) * c.d);
+    k_uniform_embedding(c, cfg.seed, 0.f, 0.f, 1);
+  } else {
+    need_embedding(c);
+    if (c.d != cfg.dim) fail(F2V_ERANGE, "embedding dim does not match cfg.dim");
+  }
+  const uint32_t n = c.n;
+  const uint32_t b = std::min(cfg.batch, n);  // trainer.cpp:200
+  const uint32_t s = cfg.negatives;
+  const ForceParams fp = make_params(cfg.model);
+  const uint64_t nb = (uint64_t(n) + b - 1) / b;
+  c.perm.ensure(sizeof(uint32_t) * n);
+  uint32_t* hperm = nullptr;
+  F2V_CUDA(cudaMallocHost(&hperm, sizeof(uint32_t) * n * 2));
+  struct Pinned {
+    uint32_t* p;
+    ~Pinned() { cudaFreeHost(p); }
+  } pin{hperm};
+  auto make_perm = [&](uint32_t e, uint32_t* out) {
+    partition_epoch(n, b, rng_keyed2(cfg.seed, kStreamPartition, e), out);
+  };
+  make_perm(cfg.first_epoch, hperm);
+  uint64_t attr = 0, rep = 0;
+  for (uint32_t e = cfg.first_epoch; e < end_epoch; ++e) {
+    uint32_t* cur_perm = hperm + size_t((e - cfg.first_epoch) & 1) * n;
+    uint32_t* nxt_perm = hperm + size_t((e - cfg.first_epoch + 1) & 1) * n;
+    float eta = cfg.lr;
+    if (cfg.lr_decay) eta = cfg.lr * (1.0f - float(e) / float(cfg.epochs));
+    F2V_CUDA(cudaMemcpyAsync(c.perm.p, cur_perm, sizeof(uint32_t) * n, cudaMemcpyHostToDevice,
+                             c.stream));
+    k_epoch_begin(c, b, s, e, cfg.seed, cfg.sampler);
+    // next epoch's Fisher-Yates overlaps this epoch's kernels
+    std::future<void> fut;
+    if (e + 1 < end_epoch)
+      fut = std::async(std::launch::async, [&, e] { make_perm(e + 1, nxt_perm); });
+    const EpochResult r = k_epoch_run(c, b, s, eta, fp, cfg.monitor_loss != 0);
+    if (fut.valid()) fut.get();
+    if (r.bad_pos != ~0ull) {
+      const uint64_t jb = r.bad_pos / b;
+      k_epoch_restore(c, b, jb);
+      const uint32_t v = cur_perm[r.bad_pos];
+      if (failure) {
+        failure->epoch = e;
+        failure->batch = jb;
+        failure->vertex = v;
+      }
+      fail(F2V_ENUMERICAL, "non-finite gradient for vertex " + std::to_string(v) + " (epoch " +
+                               std::to_string(e) + ", batch " + std::to_string(jb) + ")");
+    }
+    if (cfg.monitor_loss && loss_out) loss_out[e - cfg.first_epoch] = r.loss;
+    attr += c.nnz;            // one-hop: every arc once per epoch (trainer.cpp:154-160)
+    rep += uint64_t(n) * s;   // b*s per batch (trainer.cpp:161-162)
+  }
+  (void)nb;
+  if (counters) {
+    counters->attractive_evals += attr;
+    counters->repulsive_evals += rep;
+  }
+}
+
+}  // namespace f2v
+
+using namespace f2v;
+
+struct f2v_ctx {
+  Ctx c;
+};
+
+extern "C" {
+
+f2v_ctx* f2v_create(int32_t device) {
+  f2v_ctx* h = nullptr;
+  const int32_t rc = guard(nullptr, [&] {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+      fail(F2V_ECUDA, "no CUDA device available (there is no CPU fallback)");
+    if (device < 0 || device >= count) fail(F2V_EUSAGE, "device ordinal out of range");
+    F2V_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    F2V_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+      fail(F2V_ECUDA, std::string("device ") + prop.name + " is not sm_100 (Blackwell)");
+    h = new f2v_ctx();
+    h->c.device = device;
+    h->c.num_sms = prop.multiProcessorCount;
+    F2V_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
+    if (const char* e = std::getenv("F2V_CHUNK")) h->c.tune.chunk = std::max(1, std::atoi(e));
+  });
+  if (rc != F2V_OK) {
+    delete h;
+    return nullptr;
+  }
+  return h;
+}
+
+void f2v_destroy(f2v_ctx* h) {
+  if (!h) return;
+  cudaSetDevice(h->c.device);
+  Ctx& c = h->c;
+  for (DeviceBuf* b : {&c.rowptr, &c.col, &c.part_off, &c.chunk_cnt, &c.z[0], &c.z[1], &c.grads,
+                       &c.ids, &c.negs, &c.vloss, &c.bad, &c.scratch, &c.perm, &c.state,
+                       &c.negs_all, &c.items, &c.cnt, &c.off, &c.scan_tmp, &c.partials,
+                       &c.partial_loss, &c.ploss, &c.counters, &c.eloss})
+    b->release();
+  for (cudaEvent_t e : c.ev_kernel) cudaEventDestroy(e);
+  if (c.ev_begin) cudaEventDestroy(c.ev_begin);
+  if (c.ev_end) cudaEventDestroy(c.ev_end);
+  if (c.stream) cudaStreamDestroy(c.stream);
+  delete h;
+}
+
+const char* f2v_last_error(const f2v_ctx* h) { return h ? h->c.err.c_str() : ""; }
+
+int32_t f2v_last_timing(const f2v_ctx* h, double* out4) {
+  if (!h) return F2V_EUSAGE;
+  for (int i = 0; i < 4; ++i) out4[i] = h->c.timing[i];
+  return F2V_OK;
+}
+const char* f2v_global_error(void) { return g_global_err.c_str(); }
+
+uint64_t f2v_kernel_launches(const f2v_ctx* h, int32_t reset) {
+  if (!h) return 0;
+  const uint64_t v = h->c.launches;
+  if (reset) const_cast<f2v_ctx*>(h)->c.launches = 0;
+  return v;
+}
+
+int32_t f2v_upload_graph(f2v_ctx* h, uint32_t n, const uint64_t* row_offsets,
+                         const uint32_t* col_indices, uint64_t nnz) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    F2V_CUDA(cudaSetDevice(c.device));
+    if (row_offsets[0] != 0 || row_offsets[n] != nnz)
+      fail(F2V_ERANGE, "row_offsets inconsistent with nnz");
+    c.n = n;
+    c.nnz = nnz;
+    c.h_rowptr.assign(row_offsets, row_offsets + n + 1);
+    c.rowptr.ensure(sizeof(uint64_t) * (n + 1));
+    c.col.ensure(sizeof(uint32_t) * std::max<uint64_t>(nnz, 1));
+    F2V_CUDA(cudaMemcpyAsync(c.rowptr.p, row_offsets, sizeof(uint64_t) * (n + 1),
+                             cudaMemcpyHostToDevice, c.stream));
+    if (nnz)
+      F2V_CUDA(cudaMemcpyAsync(c.col.p, col_indices, sizeof(uint32_t) * nnz,
+                               cudaMemcpyHostToDevice, c.stream));
+    k_prepare_graph(c);
+  });
+}
+
+int32_t f2v_set_embedding(f2v_ctx* h, const float* z, uint32_t n, uint32_t d) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    F2V_CUDA(cudaSetDevice(c.device));
+    if (c.rowptr.p && n != c.n) fail(F2V_ERANGE, "embedding rows do not match the graph");
+    if (d < 1) fail(F2V_EUSAGE, "dim must be >= 1");
+    c.n = n;
+    c.d = d;
+    c.cur = 0;
+    c.z[0].ensure(sizeof(float) * size_t(n) * d);
+    F2V_CUDA(cudaMemcpyAsync(c.z[0].p, z, sizeof(float) * size_t(n) * d, cudaMemcpyHostToDevice,
+                             c.stream));
+    F2V_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int32_t f2v_get_embedding(f2v_ctx* h, float* z) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    need_embedding(c);
+    F2V_CUDA(cudaSetDevice(c.device));
+    F2V_CUDA(cudaMemcpyAsync(z, c.zcur(), sizeof(float) * size_t(c.n) * c.d,
+                             cudaMemcpyDeviceToHost, c.stream));
+    F2V_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+static int32_t device_init(f2v_ctx* h, uint32_t n, uint32_t d, uint64_t seed, float lo, float hi,
+                           int keyed) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    F2V_CUDA(cudaSetDevice(c.device));
+    if (n < 1 || d < 1) fail(F2V_EUSAGE, "init_embedding: n and d must be >= 1");
+    if (c.rowptr.p && n != c.n) fail(F2V_ERANGE, "embedding rows do not match the graph");
+    c.n = n;
+    c.d = d;
+    c.cur = 0;
+    c.z[0].ensure(sizeof(float) * size_t(n) * d);
+    k_uniform_embedding(c, seed, lo, hi, keyed);
+    F2V_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int32_t f2v_init_embedding(f2v_ctx* h, uint32_t n, uint32_t d, uint64_t seed) {
+  return device_init(h, n, d, seed, 0.f, 0.f, 1);
+}
+
+int32_t f2v_uniform_embedding(f2v_ctx* h, uint32_t n, uint32_t d, uint64_t seed, float lo,
+                              float hi) {
+  return device_init(h, n, d, seed, lo, hi, 0);
+}
+
+int32_t f2v_grad_minibatch(f2v_ctx* h, const uint32_t* ids, uint32_t b, const uint32_t* negs,
+                           uint32_t s, f2v_force_model model, float* grads_out,
+                           f2v_counters* counters, uint32_t* bad_vertex) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    need_graph(c);
+    need_embedding(c);
+    validate_model(model);
+    F2V_CUDA(cudaSetDevice(c.device));
+    stage_batch(c, ids, b, negs, s);
+    k_grad_minibatch(c, b, s, make_params(model), false);
+    c.staged_b = b;
+    const uint64_t bad = read_bad(c);
+    if (grads_out && b) {
+      F2V_CUDA(cudaMemcpyAsync(grads_out, c.grads.p, sizeof(float) * size_t(b) * c.d,
+                               cudaMemcpyDeviceToHost, c.stream));
+      F2V_CUDA(cudaStreamSynchronize(c.stream));
+    }
+    if (bad != ~0ull) {
+      if (bad_vertex) *bad_vertex = ids[bad];
+      fail(F2V_ENUMERICAL, "non-finite gradient for vertex " + std::to_string(ids[bad]));
+    }
+    if (counters) {
+      counters->attractive_evals += degree_sum(c, ids, b);
+      counters->repulsive_evals += uint64_t(b) * s;
+    }
+  });
+}
+
+int32_t f2v_apply_update(f2v_ctx* h, const uint32_t* ids, uint32_t b, const float* grads,
+                         float eta) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    need_embedding(c);
+    F2V_CUDA(cudaSetDevice(c.device));
+    if (!grads && b != c.staged_b) fail(F2V_EUSAGE, "no staged gradient of this batch size");
+    for (uint32_t i = 0; i < b; ++i)
+      if (ids[i] >= c.n) fail(F2V_ERANGE, "vertex id out of range");
+    c.ids.ensure(sizeof(uint32_t) * std::max<uint32_t>(b, 1));
+    c.grads.ensure(sizeof(float) * std::max<size_t>(size_t(b) * c.d, 1));
+    F2V_CUDA(cudaMemcpyAsync(c.ids.p, ids, sizeof(uint32_t) * b, cudaMemcpyHostToDevice,
+                             c.stream));
+    if (grads)
+      F2V_CUDA(cudaMemcpyAsync(c.grads.p, grads, sizeof(float) * size_t(b) * c.d,
+                               cudaMemcpyHostToDevice, c.stream));
+    std::vector<uint32_t> sorted(ids, ids + b);
+    std::sort(sorted.begin(), sorted.end());
+    const bool uniq = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+    k_apply_update(c, b, eta, uniq);
+    F2V_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int32_t f2v_batch_loss(f2v_ctx* h, const uint32_t* ids, uint32_t b, const uint32_t* negs,
+                       uint32_t s, f2v_force_model model, double* loss_out) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    need_graph(c);
+    need_embedding(c);
+    validate_model(model);
+    if (model.kind != F2V_SIGMOID && model.kind != F2V_TDIST)
+      fail(F2V_EUNSUPPORTED, "batch_loss is defined for sigmoid and tdist only");
+    F2V_CUDA(cudaSetDevice(c.device));
+    stage_batch(c, ids, b, negs, s);
+    k_grad_minibatch(c, b, s, make_params(model), true);
+    c.staged_b = 0;  // the staged gradient is not a requested one
+    *loss_out = b ? k_batch_loss_sum(c, b) : 0.0;
+  });
+}
+
+int32_t f2v_step(f2v_ctx* h, const uint32_t* ids, uint32_t b, const uint32_t* negs, uint32_t s,
+                 f2v_force_model model, float eta, double* loss_out, f2v_counters* counters,
+                 uint32_t* bad_vertex) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    need_graph(c);
+    need_embedding(c);
+    validate_model(model);
+    const bool mon = loss_out != nullptr;
+    if (mon && model.kind != F2V_SIGMOID && model.kind != F2V_TDIST)
+      fail(F2V_EUNSUPPORTED, "batch_loss is defined for sigmoid and tdist only");
+    F2V_CUDA(cudaSetDevice(c.device));
+    const bool uniq = stage_batch(c, ids, b, negs, s);
+    k_grad_minibatch(c, b, s, make_params(model), mon);
+    const uint64_t bad = read_bad(c);
+    if (bad != ~0ull) {  // thrown before apply_update: Z untouched (trainer.cpp:149-152)
+      if (bad_vertex) *bad_vertex = ids[bad];
+      fail(F2V_ENUMERICAL, "non-finite gradient for vertex " + std::to_string(ids[bad]));
+    }
+    if (mon) *loss_out = b ? k_batch_loss_sum(c, b) : 0.0;
+    k_apply_update(c, b, eta, uniq);
+    c.staged_b = b;
+    F2V_CUDA(cudaStreamSynchronize(c.stream));
+    if (counters) {
+      counters->attractive_evals += degree_sum(c, ids, b);
+      counters->repulsive_evals += uint64_t(b) * s;
+    }
+  });
+}
+
+int32_t f2v_train_epochs(f2v_ctx* h, const f2v_train_config* cfg, double* loss_out,
+                         f2v_counters* counters, f2v_failure* failure) {
+  return guard(&h->c, [&] {
+    F2V_CUDA(cudaSetDevice(h->c.device));
+    train_epochs(h->c, *cfg, loss_out, counters, failure);
+  });
+}
+
+int32_t f2v_train(int32_t device, uint32_t n, const uint64_t* row_offsets,
+                  const uint32_t* col_indices, uint64_t nnz, float* z_inout,
+                  const f2v_train_config* cfg, double* loss_out, f2v_counters* counters,
+                  f2v_failure* failure) {
+  f2v_ctx* h = f2v_create(device);
+  if (!h) return F2V_ECUDA;
+  int32_t rc = f2v_upload_graph(h, n, row_offsets, col_indices, nnz);
+  if (rc == F2V_OK && cfg->init != 1) rc = f2v_set_embedding(h, z_inout, n, cfg->dim);
+  if (rc == F2V_OK) {
+    rc = f2v_train_epochs(h, cfg, loss_out, counters, failure);
+    // Z after the last complete batch, also on F2V_ENUMERICAL
+    if (rc == F2V_OK || rc == F2V_ENUMERICAL) {
+      const int32_t rc2 = f2v_get_embedding(h, z_inout);
+      if (rc == F2V_OK) rc = rc2;
+    }
+  }
+  if (rc != F2V_OK) g_global_err = h->c.err;
+  f2v_destroy(h);
+  return rc;
+}
+
+int32_t f2v_csr_from_edges(const uint32_t* pairs, uint64_t m, uint32_t n, int32_t symmetrize,
+                           uint64_t* row_offsets_out, uint32_t* col_out, uint64_t* nnz_out,
+                           uint64_t* duplicates_dropped, uint64_t* self_loops_dropped) {
+  return guard(nullptr, [&] {
+    csr_from_edges(pairs, m, n, symmetrize != 0, row_offsets_out, col_out, nnz_out,
+                   duplicates_dropped, self_loops_dropped);
+  });
+}
+
+int32_t f2v_partition_epoch(uint32_t n, uint32_t b, uint64_t seed, uint32_t epoch,
+                            uint32_t* perm_out) {
+  return guard(nullptr, [&] {
+    partition_epoch(n, b, rng_keyed2(seed, kStreamPartition, epoch), perm_out);
+  });
+}
+
+int32_t f2v_negatives(int32_t sampler, uint64_t seed, uint32_t epoch, uint64_t batch,
+                      uint32_t shard, uint32_t num_shards, uint32_t n, uint32_t s,
+                      uint32_t* out) {
+  return guard(nullptr, [&] {
+    if (n < 1) fail(F2V_EUSAGE, "n must be >= 1");
+    for (uint32_t k = 0; k < s; ++k)
+      out[k] = sampler == F2V_SAMPLER_PHILOX
+                   ? philox_negative(seed, epoch, batch, shard, k, n)
+                   : splitmix_negative(seed, epoch, batch, shard, std::max(1u, num_shards), k, n);
+  });
+}
+
+static int32_t emit(std::vector<uint32_t>&& e, uint32_t** pairs_out, uint64_t* m_out) {
+  uint32_t* p = static_cast<uint32_t*>(std::malloc(sizeof(uint32_t) * std::max<size_t>(e.size(), 2)));
+  if (!p) return F2V_ECUDA;
+  std::memcpy(p, e.data(), sizeof(uint32_t) * e.size());
+  *pairs_out = p;
+  *m_out = e.size() / 2;
+  return F2V_OK;
+}
+
+int32_t f2v_gen_sbm(uint32_t n, int32_t blocks, double p_in, double p_out, uint64_t seed,
+                    uint32_t** pairs_out, uint64_t* m_out) {
+  int32_t rc2 = F2V_OK;
+  const int32_t rc = guard(nullptr, [&] {
+    rc2 = emit(gen_sbm(n, blocks, p_in, p_out, seed), pairs_out, m_out);
+  });
+  return rc ? rc : rc2;
+}
+
+int32_t f2v_gen_rmat(uint32_t scale, uint32_t ef, double a, double b, double c, uint64_t seed,
+                     uint32_t** pairs_out, uint64_t* m_out) {
+  int32_t rc2 = F2V_OK;
+  const int32_t rc = guard(nullptr, [&] {
+    rc2 = emit(gen_rmat(scale, ef, a, b, c, seed), pairs_out, m_out);
+  });
+  return rc ? rc : rc2;
+}
+
+int32_t f2v_gen_chung_lu(uint32_t n, double expo, double min_deg, double max_deg,
+                         double mean_deg, uint64_t seed, uint32_t** pairs_out, uint64_t* m_out) {
+  int32_t rc2 = F2V_OK;
+  const int32_t rc = guard(nullptr, [&] {
+    rc2 = emit(gen_chung_lu(n, expo, min_deg, max_deg, mean_deg, seed), pairs_out, m_out);
+  });
+  return rc ? rc : rc2;
+}
+
+int32_t f2v_gen_rgg(uint32_t n, double mean_deg, uint64_t seed, uint32_t** pairs_out,
+                    uint64_t* m_out) {
+  int32_t rc2 = F2V_OK;
+  const int32_t rc = guard(nullptr, [&] {
+    rc2 = emit(gen_rgg(n, mean_deg, seed), pairs_out, m_out);
+  });
+  return rc ? rc : rc2;
+}
+
+void f2v_free(void* p) { std::free(p); }
+
+}  // extern "C"

@@ -1,0 +1,108 @@
+// f2v_internal.h -- device context shared by the C-ABI (f2v_capi.cpp), the
+// host driver (f2v_host.cpp) and the kernels (f2v_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/force2vec_b200.h"
+
+namespace f2v {
+
+// Error raised inside the library; carries the C-ABI code.
+struct Error {
+  int32_t code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int32_t code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+#define F2V_CUDA(x) ::f2v::cuda_check((x), #x)
+
+// Per-pair model parameters in the form the kernels use.
+struct ForceParams {
+  int32_t kind;
+  int32_t has_cap;
+  double eps;  // double(model.epsilon)   (force_kernels.cpp:105,113)
+  double cap;  // double(*repulsion_cap)  (force_kernels.cpp:72)
+};
+
+struct DeviceBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t want);
+  void release();
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+// Tunables of the dataflow epoch kernel.
+struct EpochTuning {
+  uint32_t chunk = 256;        // max arcs per work item (hub splitting)
+  uint32_t threads = 256;      // CTA size
+  uint32_t claim = 1;          // items claimed per atomic
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  std::string err;
+  uint64_t launches = 0;
+  EpochTuning tune;
+
+  // graph (CsrGraph, csr_graph.hpp:24-101)
+  uint32_t n = 0;
+  uint64_t nnz = 0;
+  DeviceBuf rowptr, col;
+  std::vector<uint64_t> h_rowptr;  // host copy: degrees for counters/partials
+  // hub-splitting bookkeeping, static per (graph, chunk)
+  DeviceBuf part_off;    // u32[n]: first partial slot of a multi-chunk vertex
+  DeviceBuf chunk_cnt;   // u32[n]: arrival counters (self-resetting)
+  uint64_t part_slots = 0;
+  uint64_t max_items = 0;
+  uint32_t part_chunk = 0;
+
+  // embedding (EmbeddingMatrix, trainer.hpp:33-57): double-buffered for epochs
+  uint32_t d = 0;
+  DeviceBuf z[2];
+  int cur = 0;
+
+  // per-step staging (GradBuffer, trainer.hpp:59-71)
+  DeviceBuf grads, ids, negs, vloss, bad, scratch;
+  uint32_t staged_b = 0;
+
+  // epoch buffers
+  DeviceBuf perm, state, negs_all, items, cnt, off, scan_tmp, partials, partial_loss, ploss,
+      counters, eloss;
+  std::vector<uint32_t> h_perm;
+
+  // timing of the last train_epochs call (f2v_last_timing)
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  std::vector<cudaEvent_t> ev_kernel;  // pairs around each epoch kernel
+  uint32_t ev_used = 0;
+  double timing[4] = {0, 0, 0, 0};
+
+  float* zcur() const { return z[cur].as<float>(); }
+};
+
+// kernels (f2v_kernels.cu)
+void k_grad_minibatch(Ctx& c, uint32_t b, uint32_t s, const ForceParams& fp, bool want_loss);
+void k_apply_update(Ctx& c, uint32_t b, float eta, bool unique_ids);
+double k_batch_loss_sum(Ctx& c, uint32_t b);
+void k_uniform_embedding(Ctx& c, uint64_t seed, float lo, float hi, int keyed_init);
+// one device-resident epoch; returns the first failing perm position or UINT64_MAX
+struct EpochResult {
+  uint64_t bad_pos;
+  double loss;
+};
+void k_prepare_graph(Ctx& c);
+void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed, int sampler);
+EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForceParams& fp,
+                        bool monitor);
+void k_epoch_restore(Ctx& c, uint32_t b, uint64_t bad_batch);
+
+ForceParams make_params(const f2v_force_model& m);
+
+}  // namespace f2v
