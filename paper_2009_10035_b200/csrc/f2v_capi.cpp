@@ -251,7 +251,7 @@ f2v_ctx* f2v_create(int32_t device) {
     h->c.device = device;
     h->c.num_sms = prop.multiProcessorCount;
     F2V_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
-    if (const char* e = std::getenv("F2V_CHUNK")) h->c.tune.chunk = std::max(1, std::atoi(e));
+    load_tuning(h->c.tune);
   });
   if (rc != F2V_OK) {
     delete h;
@@ -264,10 +264,11 @@ void f2v_destroy(f2v_ctx* h) {
   if (!h) return;
   cudaSetDevice(h->c.device);
   Ctx& c = h->c;
-  for (DeviceBuf* b : {&c.rowptr, &c.col, &c.part_off, &c.chunk_cnt, &c.z[0], &c.z[1], &c.grads,
-                       &c.ids, &c.negs, &c.vloss, &c.bad, &c.scratch, &c.perm, &c.state,
-                       &c.negs_all, &c.items, &c.cnt, &c.off, &c.scan_tmp, &c.partials,
-                       &c.partial_loss, &c.ploss, &c.counters, &c.eloss})
+  for (DeviceBuf* b :
+       {&c.rowptr, &c.col, &c.cbase, &c.lbase, &c.lpo, &c.ecnt, &c.lcnt, &c.vflag, &c.z[0], &c.z[1],
+        &c.grads, &c.ids, &c.negs, &c.vloss, &c.bad, &c.scratch, &c.perm, &c.state, &c.negs_all,
+        &c.negwin, &c.items, &c.nE, &c.nL, &c.EP, &c.LP, &c.sz, &c.SS, &c.scan_tmp, &c.epart,
+        &c.eloss, &c.wcnt, &c.wl, &c.lpart, &c.lloss, &c.ploss, &c.counters})
     b->release();
   for (cudaEvent_t e : c.ev_kernel) cudaEventDestroy(e);
   if (c.ev_begin) cudaEventDestroy(c.ev_begin);

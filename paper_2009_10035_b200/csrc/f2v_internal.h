@@ -37,12 +37,16 @@ struct DeviceBuf {
   template <class T> T* as() const { return static_cast<T*>(p); }
 };
 
-// Tunables of the dataflow epoch kernel.
+// Tunables of the dataflow epoch kernel; each can
+// be overridden by the environment variable named beside it.
 struct EpochTuning {
-  uint32_t chunk = 256;        // max arcs per work item (hub splitting)
-  uint32_t threads = 256;      // CTA size
-  uint32_t claim = 1;          // items claimed per atomic
+  uint32_t chunk = 256;     // F2V_CHUNK: max arcs per E item (hub splitting)
+  uint32_t lgroup = 8;      // F2V_LGROUP: E chunks per L item
+  uint32_t lookahead = 32;  // F2V_LOOKAHEAD: E items run this many batches ahead
+  uint32_t window = 48;     // F2V_WINDOW: arcs to batches [j-window, j) wait for L
+  uint32_t recent = 2;      // F2V_RECENT: window arcs this recent are taken last
 };
+void load_tuning(EpochTuning& t);
 
 struct Ctx {
   int device = 0;
@@ -57,12 +61,10 @@ struct Ctx {
   uint64_t nnz = 0;
   DeviceBuf rowptr, col;
   std::vector<uint64_t> h_rowptr;  // host copy: degrees for counters/partials
-  // hub-splitting bookkeeping, static per (graph, chunk)
-  DeviceBuf part_off;    // u32[n]: first partial slot of a multi-chunk vertex
-  DeviceBuf chunk_cnt;   // u32[n]: arrival counters (self-resetting)
-  uint64_t part_slots = 0;
-  uint64_t max_items = 0;
-  uint32_t part_chunk = 0;
+  // chunk / L-group layout, static per (graph, chunk, lgroup)
+  DeviceBuf cbase, lbase, lpo, ecnt, lcnt, vflag;
+  uint64_t chunks = 0, lgroups = 0, lslots = 0;
+  uint32_t prepared_chunk = 0, prepared_lgroup = 0;
 
   // embedding (EmbeddingMatrix, trainer.hpp:33-57): double-buffered for epochs
   uint32_t d = 0;
@@ -74,9 +76,8 @@ struct Ctx {
   uint32_t staged_b = 0;
 
   // epoch buffers
-  DeviceBuf perm, state, negs_all, items, cnt, off, scan_tmp, partials, partial_loss, ploss,
-      counters, eloss;
-  std::vector<uint32_t> h_perm;
+  DeviceBuf perm, state, negs_all, negwin, items, nE, nL, EP, LP, sz, SS, scan_tmp, epart, eloss,
+      wcnt, wl, lpart, lloss, ploss, counters;
 
   // timing of the last train_epochs call (f2v_last_timing)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;

@@ -1,0 +1,288 @@
+// f2v_pair.cuh -- the per-pair force math of force_kernels.cpp:30-169 and the
+// warp-level row accumulation shared by the step and epoch kernels.
+//
+// Layout: Z is row-major f32[n x d]; one warp owns
+// one batch row; lane L holds K columns of every row it touches (VEC layout:
+// columns [L*K, L*K+K), one 16-byte load per lane for d = 128), so a
+// neighbour row is one fully coalesced 512-byte gather.  Dot products /
+// distances are fp64 (warp butterfly), the per-pair term and the per-vertex
+// accumulator are fp64 exactly as force_kernels.cpp:30-77 and
+// trainer.cpp:124-138 compute them; every multiply and add is an explicit
+// __d*_rn so the separate roundings of the reference survive (the files are
+// also compiled with --fmad=false).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "f2v_internal.h"
+
+namespace f2v {
+namespace dev {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kNewBit = 0x80000000u;
+
+// Relaxed (no L1 invalidation) global loads/stores for cross-warp flags; the
+// data they guard is always read through L2 (ld.cg) after the flag is seen.
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// force_kernels.hpp:25-29
+__device__ __forceinline__ double stable_sigmoid(double x) {
+  if (x >= 0) return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
+  const double e = exp(x);
+  return __ddiv_rn(e, __dadd_rn(1.0, e));
+}
+
+__device__ __forceinline__ double dmax(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint32_t umin32(uint32_t a, uint32_t b) { return a < b ? a : b; }
+
+// ---------------------------------------------------------------- row I/O
+// K columns per lane. VEC: columns lane*K..lane*K+K-1 (d == 32*K exactly,
+// vector loads). !VEC: columns k*32+lane, masked by d (any d <= 32*K).
+template <int K, bool VEC>
+struct Lay {
+  __device__ static __forceinline__ uint32_t col(int lane, int k) {
+    return VEC ? uint32_t(lane * K + k) : uint32_t(k * 32 + lane);
+  }
+  __device__ static __forceinline__ bool valid(int lane, int k, uint32_t d) {
+    return VEC ? true : (uint32_t(k * 32 + lane) < d);
+  }
+  // coherent = row may have been written during this launch (L2 path)
+  __device__ static __forceinline__ void load(const float* row, int lane, uint32_t d,
+                                              float (&v)[K], bool coherent) {
+    if constexpr (VEC && K % 4 == 0) {
+#pragma unroll
+      for (int q = 0; q < K / 4; ++q) {
+        const float4* p = reinterpret_cast<const float4*>(row + lane * K) + q;
+        const float4 t = coherent ? __ldcg(p) : __ldg(p);
+        v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+      }
+    } else if constexpr (VEC && K == 2) {
+      const float2* p = reinterpret_cast<const float2*>(row + lane * 2);
+      const float2 t = coherent ? __ldcg(p) : __ldg(p);
+      v[0] = t.x; v[1] = t.y;
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t c = col(lane, k);
+        v[k] = (VEC || c < d) ? (coherent ? __ldcg(row + c) : __ldg(row + c)) : 0.0f;
+      }
+    }
+  }
+  __device__ static __forceinline__ void store(float* row, int lane, uint32_t d,
+                                               const float (&v)[K]) {
+    if constexpr (VEC && K % 4 == 0) {
+#pragma unroll
+      for (int q = 0; q < K / 4; ++q)
+        __stcg(reinterpret_cast<float4*>(row + lane * K) + q,
+               make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        if (valid(lane, k, d)) __stcg(row + col(lane, k), v[k]);
+    }
+  }
+  // fp64 accumulator rows (hub partials): plain coalesced L2 stores / loads
+  __device__ static __forceinline__ void store_acc(double* row, int lane, uint32_t d,
+                                                   const double (&a)[K]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (valid(lane, k, d)) __stcg(row + col(lane, k), a[k]);
+  }
+  __device__ static __forceinline__ void load_acc(const double* row, int lane, uint32_t d,
+                                                  double (&a)[K]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) a[k] = valid(lane, k, d) ? __ldcg(row + col(lane, k)) : 0.0;
+  }
+  __device__ static __forceinline__ void add_acc(const double* row, int lane, uint32_t d,
+                                                 double (&a)[K]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (valid(lane, k, d)) a[k] = __dadd_rn(a[k], __ldcg(row + col(lane, k)));
+  }
+};
+
+// ------------------------------------------------------- per-pair terms
+// Scalar part of one pair: out_j = coef * o_j              (sigmoid)
+//                          out_j = coef * (u_j - o_j) * inv (distance kinds)
+//                          out   = (coef, 0, ..., 0)       (coincident fallback)
+// followed by  out_j *= scale  when clamped (force_kernels.cpp:69-77).
+struct Term {
+  double coef, inv, scale;
+  bool dist, fallback, clamped;
+  double loss;
+};
+
+// red = <u,o> (sigmoid) or ||u-o||^2 (distance kinds); nw2 = ||o||^2 for the
+// clamped sigmoid repulsion (force_kernels.cpp:95).
+template <bool MON>
+__device__ __forceinline__ Term pair_term(const ForceParams& fp, bool attractive, double red,
+                                          double nw2) {
+  Term t{};
+  t.scale = 1.0;
+  if (fp.kind == F2V_SIGMOID) {  // force_kernels.cpp:79-97
+    const double x = red;
+    const double sg = stable_sigmoid(x);
+    t.coef = attractive ? __dsub_rn(sg, 1.0) : sg;
+    if (!attractive && fp.has_cap) {
+      const double m = __dmul_rn(t.coef, sqrt(nw2));
+      t.clamped = !(m <= fp.cap || m == 0.0);
+      if (t.clamped) t.scale = __ddiv_rn(fp.cap, m);
+    }
+    if (MON) {  // force_kernels.cpp:213-219
+      if (attractive)
+        t.loss = x >= 0 ? log1p(exp(-x)) : __dadd_rn(-x, log1p(exp(x)));
+      else
+        t.loss = x >= 0 ? __dadd_rn(x, log1p(exp(-x))) : log1p(exp(x));
+    }
+    return t;
+  }
+  t.dist = true;
+  const double r_raw = sqrt(red);  // distance(), force_kernels.cpp:36-43
+  double scalar;
+  bool clamp_it = false;
+  if (fp.kind == F2V_TDIST) {
+    if (attractive) {  // 99-107
+      scalar = __ddiv_rn(__dmul_rn(2.0, r_raw), __dadd_rn(1.0, __dmul_rn(r_raw, r_raw)));
+    } else {  // 109-119
+      const double tt = dmax(r_raw, fp.eps);
+      scalar = __ddiv_rn(-2.0, __dmul_rn(tt, __dadd_rn(1.0, __dmul_rn(tt, tt))));
+      clamp_it = true;
+    }
+    if (MON) {  // force_kernels.cpp:221-227
+      const double t2 = __dmul_rn(r_raw, r_raw);
+      if (attractive) {
+        t.loss = log1p(t2);
+      } else {
+        const double tc = dmax(t2, __dmul_rn(fp.eps, fp.eps));
+        t.loss = -log(__ddiv_rn(tc, __dadd_rn(1.0, tc)));
+      }
+    }
+  } else {  // table-II kinds, force_kernels.cpp:121-147
+    if (attractive) {
+      scalar = fp.kind == F2V_FR ? __dmul_rn(r_raw, r_raw)
+                                 : (fp.kind == F2V_FA ? r_raw : log1p(r_raw));
+    } else {
+      scalar = __ddiv_rn(-1.0, dmax(r_raw, fp.eps));
+      clamp_it = true;
+    }
+  }
+  t.coef = scalar;
+  t.fallback = r_raw < fp.eps;  // scaled_unit_diff, force_kernels.cpp:54-65
+  t.inv = __ddiv_rn(1.0, r_raw);
+  if (clamp_it && fp.has_cap) {
+    const double m = fabs(scalar);
+    t.clamped = !(m <= fp.cap || m == 0.0);
+    if (t.clamped) t.scale = __ddiv_rn(fp.cap, m);
+  }
+  return t;
+}
+
+// acc += out(term) with the reference's rounding sequence.  w = the other
+// row (sigmoid) or u - other (distance kinds), both exact in fp64.
+template <int K>
+__device__ __forceinline__ void accumulate(const Term& t, int lane, const double (&w)[K],
+                                           double (&acc)[K]) {
+  if (!t.dist) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double o = __dmul_rn(t.coef, w[k]);
+      if (t.clamped) o = __dmul_rn(o, t.scale);
+      acc[k] = __dadd_rn(acc[k], o);
+    }
+    return;
+  }
+  if (t.fallback) {
+    if (lane == 0) {  // column 0 lives on lane 0, k = 0 in both layouts
+      double o = t.coef;
+      if (t.clamped) o = __dmul_rn(o, t.scale);
+      acc[0] = __dadd_rn(acc[0], o);
+    }
+    // the other columns add +0.0 (or +0.0*scale): acc + 0.0 == acc except -0.0
+    const double zero = t.clamped ? __dmul_rn(0.0, t.scale) : 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (lane != 0 || k != 0) acc[k] = __dadd_rn(acc[k], zero);
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double o = __dmul_rn(__dmul_rn(t.coef, w[k]), t.inv);
+    if (t.clamped) o = __dmul_rn(o, t.scale);
+    acc[k] = __dadd_rn(acc[k], o);
+  }
+}
+
+// Accumulate the pairs of `cnt` (<= 32) other-rows whose packed ids sit one per
+// lane (bit 31 = read the coherent Znew buffer), in lane order, U at a time.
+// Each row is converted to fp64 once and reused by the reduction and the axpy.
+template <int K, bool VEC, int U, bool MON, bool ATT>
+__device__ __forceinline__ void accumulate_rows(const ForceParams& fp, uint32_t packed, int cnt,
+                                                int lane, uint32_t d,
+                                                const float* __restrict__ zold,
+                                                const float* __restrict__ znew,
+                                                const double (&uu)[K], double (&acc)[K],
+                                                double& lsum) {
+  using L = Lay<K, VEC>;
+  const bool sig = fp.kind == F2V_SIGMOID;
+  for (int k0 = 0; k0 < cnt; k0 += U) {
+    float v[U][K];
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
+      if (k0 + i < cnt) {
+        const bool coh = (pk & kNewBit) != 0;
+        L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, v[i], coh);
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[i][k] = 0.0f;
+      }
+    }
+    double w[U][K], red[U], nw[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      double s = 0.0, q = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const double o = double(v[i][k]);
+        if (sig) {
+          w[i][k] = o;
+          s = __dadd_rn(s, __dmul_rn(uu[k], o));
+          if (!ATT) q = __dadd_rn(q, __dmul_rn(o, o));
+        } else {
+          w[i][k] = __dsub_rn(uu[k], o);
+          s = __dadd_rn(s, __dmul_rn(w[i][k], w[i][k]));
+        }
+      }
+      red[i] = s;
+      nw[i] = q;
+    }
+#pragma unroll
+    for (int m = 16; m; m >>= 1) {
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        red[i] = __dadd_rn(red[i], __shfl_xor_sync(kFull, red[i], m));
+        if (!ATT && sig) nw[i] = __dadd_rn(nw[i], __shfl_xor_sync(kFull, nw[i], m));
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+      if (k0 + i < cnt) {
+        const Term t = pair_term<MON>(fp, ATT, red[i], nw[i]);
+        accumulate<K>(t, lane, w[i], acc);
+        if (MON) lsum = __dadd_rn(lsum, t.loss);
+      }
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace f2v
