@@ -8,19 +8,23 @@
 // batch j must see row v as of the end of batch j-1, i.e. Znew[v] iff
 // batch(v) < j, else Zold[v].  state[v] = batch(v) << 1 | written.
 //
-// Schedule.  Each vertex's work is split into
-//   E items (one per C-arc chunk of its CSR row): arcs to rows that are either
-//     in batches >= j (Zold, no dependency) or "past" (batch < j - W, final long
-//     ago).  The remaining "window" arcs (j - W <= batch(v) < j) are compacted
-//     into a per-chunk list.  A vertex with no window arcs and no window
-//     negatives is finalised right here.
-//   L items (one per G chunks): the window arcs, oldest first, then the
-//     most recent (age <= R) last, waiting on each row's written bit; combine
-//     with the E partial + the shared negatives; finalise.
-// Items are claimed in a static order where the E items of batch t sit next to
-// the L items of batch t - A (lookahead A < W): the bandwidth-heavy E work
-// runs A batches ahead of the latency-critical L chain, and every wait points
-// at an item claimed earlier (deadlock-free on any number of resident CTAs).
+// Work split.  Arcs (u, v) of a batch-j vertex fall in three classes:
+//   early   batch(v) >= j        -> Zold, no dependency;
+//   past    batch(v) <  j - W    -> Znew, final long before u's turn;
+//   window  j - W <= batch(v) < j -> Znew, on the dependency chain.
+// E items (one per C-arc chunk, bandwidth-heavy) take early + past arcs and
+// compact the window arcs into a per-chunk list.  A per-epoch pre-scan marks
+// the vertices that have window arcs or window negatives ("needs L"); every
+// other vertex is finalised by its E item.  L items (one per G chunks of a
+// needs-L vertex, latency-critical) take the E partial, the window arcs with
+// age > R, the shared negatives, then the most recent window arcs, waiting
+// on each row's written bit, and finalise.
+//
+// Warp roles.  Every CTA has E warps and L warps with their own claim
+// counters over statically ordered (batch-major) item lists.  Each list is
+// claimed in order and every wait points at an item that is lower in the
+// global (batch, E-before-L) order, so the lowest unfinished item is always
+// claimed and runnable: deadlock-free on any number of resident CTAs.
 // Partials of split rows are combined in a fixed order by the last arrival
 // (no float atomics): results are bitwise reproducible run to run.
 #include <cub/device/device_scan.cuh>
@@ -42,8 +46,9 @@ namespace {
 
 using namespace dev;
 
-constexpr uint32_t kLBit = 0x80000000u;
-constexpr int kU = 4;  // rows in flight per warp per accumulate step
+constexpr int kU = 4;           // rows in flight per warp per accumulate step
+constexpr int kWarps = 8;       // warps per CTA
+constexpr int kQ = 64;          // per-warp compaction queue (entries)
 
 struct EpochArgs {
   const uint64_t* rowptr;
@@ -54,12 +59,15 @@ struct EpochArgs {
   uint32_t* state;
   const uint32_t* negs;
   const uint32_t* negwin;
-  const uint2* items;
-  uint32_t nitems;
-  uint32_t* next;
+  const uint2* eitems;
+  const uint2* litems;
+  uint32_t n_eitems;
+  const uint32_t* n_litems;  // device count (written by the prep)
+  uint32_t* next;  // [0] E claims, [1] L claims
   const uint32_t* cbase;
   const uint32_t* lbase;
   const uint32_t* lpo;
+  const uint32_t* needs;  // per vertex: window arcs/negatives exist
   double* epart;
   double* eloss;
   uint32_t* wcnt;
@@ -72,7 +80,7 @@ struct EpochArgs {
   double* ploss;
   unsigned long long* bad;
   uint32_t n, d, b, s;
-  uint32_t C, G, A, W, R;
+  uint32_t C, G, W, R, lwarps;
   float eta;
   ForceParams fp;
 };
@@ -87,17 +95,40 @@ __device__ __forceinline__ uint32_t wait_written(const uint32_t* state, uint32_t
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
-// Compact the lanes with `keep` (in lane order) into lanes 0..cnt-1.
-__device__ __forceinline__ uint32_t compact(uint32_t* sh, int lane, bool keep, uint32_t val,
-                                            int& cnt) {
-  const uint32_t m = __ballot_sync(kFull, keep);
-  if (keep) sh[__popc(m & lanemask_lt(lane))] = val;
-  __syncwarp();
-  cnt = __popc(m);
-  const uint32_t out = lane < cnt ? sh[lane] : 0u;
-  __syncwarp();
-  return out;
-}
+// Per-warp FIFO of packed row ids (bit 31 = Znew) in shared memory; rows
+// are accumulated 32 at a time in push order (= the deterministic pair order).
+template <int K, bool VEC, bool MON, bool ATT>
+struct RowQueue {
+  uint32_t* buf;
+  int n;
+  __device__ __forceinline__ void push(const EpochArgs& a, int lane, bool keep, uint32_t val,
+                                       const double (&uu)[K], double (&acc)[K], double& lsum) {
+    const uint32_t m = __ballot_sync(kFull, keep);
+    if (keep) buf[n + __popc(m & lanemask_lt(lane))] = val;
+    __syncwarp();
+    n += __popc(m);
+    if (n >= 32) {
+      const uint32_t pk = buf[lane];
+      const uint32_t rest = lane + 32 < n ? buf[lane + 32] : 0u;
+      __syncwarp();
+      buf[lane] = rest;
+      __syncwarp();
+      n -= 32;
+      accumulate_rows<K, VEC, kU, MON, ATT>(a.fp, pk, 32, lane, a.d, a.zold, a.znew, uu, acc,
+                                            lsum);
+    }
+  }
+  __device__ __forceinline__ void flush(const EpochArgs& a, int lane, const double (&uu)[K],
+                                        double (&acc)[K], double& lsum) {
+    if (n == 0) return;
+    const uint32_t pk = lane < n ? buf[lane] : 0u;
+    __syncwarp();
+    const int cnt = n;
+    n = 0;
+    accumulate_rows<K, VEC, kU, MON, ATT>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew, uu, acc,
+                                          lsum);
+  }
+};
 
 // The shared negatives of batch j, in sample order (sampling.cpp:59).
 template <int K, bool VEC, bool MON>
@@ -109,7 +140,7 @@ __device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, int
     uint32_t pk = 0;
     if (lane < cnt) {
       const uint32_t w = a.negs[size_t(j) * a.s + k0 + lane];
-      uint32_t st = ld_relaxed(a.state + w);
+      const uint32_t st = ld_relaxed(a.state + w);
       if ((st >> 1) < j) {
         wait_written(a.state, w, st);
         pk = w | kNewBit;
@@ -149,7 +180,7 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_
 }
 
 template <int K, bool VEC, bool MON>
-__device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint32_t* sh) {
+__device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint32_t* qbuf) {
   using L = Lay<K, VEC>;
   const uint32_t u = a.perm[p];
   const uint32_t j = p / a.b;
@@ -166,13 +197,14 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
   for (int k = 0; k < K; ++k) { uu[k] = zu[k]; acc[k] = 0.0; }
   double lsum = 0.0;
   uint32_t wc = 0;
+  RowQueue<K, VEC, MON, true> q{qbuf, 0};
   for (uint64_t e = e0; e < e1; e += 32) {
     const int cnt = int(umin64(32, e1 - e));
     uint32_t v = 0, pk = 0;
     bool use = false, win = false;
     if (lane < cnt) {
       v = a.col[e + lane];
-      uint32_t st = ld_relaxed(a.state + v);
+      const uint32_t st = ld_relaxed(a.state + v);
       const uint32_t bv = st >> 1;
       if (bv >= j) {
         use = true;
@@ -188,17 +220,14 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
     const uint32_t wm = __ballot_sync(kFull, win);
     if (win) a.wl[e0 + wc + __popc(wm & lanemask_lt(lane))] = v;
     wc += __popc(wm);
-    int cu;
-    const uint32_t pkc = compact(sh, lane, use, pk, cu);
-    accumulate_rows<K, VEC, kU, MON, true>(a.fp, pkc, cu, lane, a.d, a.zold, a.znew, uu, acc,
-                                           lsum);
+    q.push(a, lane, use, pk, uu, acc, lsum);
   }
-  const bool negwin = a.negwin[j] != 0;
+  q.flush(a, lane, uu, acc, lsum);
+  const bool needs = a.needs[u] != 0;
   if (nch == 1) {
-    if (wc == 0 && !negwin) {  // nothing depends on the window: finalise now
+    if (!needs) {
       do_negatives<K, VEC, MON>(a, j, lane, uu, acc, lsum);
       finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
-      if (lane == 0) st_relaxed(a.vflag + u, 2u);
     } else {
       L::store_acc(a.epart + size_t(cs) * a.d, lane, a.d, acc);
       if (lane == 0) {
@@ -225,18 +254,15 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
   __threadfence();
   L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
   lsum = MON ? __ldcg(a.eloss + cb) : 0.0;
-  uint32_t anyw = __ldcg(a.wcnt + cb);
 #pragma unroll 4
-  for (uint32_t q = 1; q < nch; ++q) {
-    L::add_acc(a.epart + size_t(cb + q) * a.d, lane, a.d, acc);
-    if (MON) lsum = __dadd_rn(lsum, __ldcg(a.eloss + cb + q));
-    anyw += __ldcg(a.wcnt + cb + q);
+  for (uint32_t qq = 1; qq < nch; ++qq) {
+    L::add_acc(a.epart + size_t(cb + qq) * a.d, lane, a.d, acc);
+    if (MON) lsum = __dadd_rn(lsum, __ldcg(a.eloss + cb + qq));
   }
   if (lane == 0) a.ecnt[u] = 0;
-  if (anyw == 0 && !negwin) {
+  if (!needs) {
     do_negatives<K, VEC, MON>(a, j, lane, uu, acc, lsum);
     finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
-    if (lane == 0) st_relaxed(a.vflag + u, 2u);
   } else {
     L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);  // the E total
     if (MON && lane == 0) __stcg(a.eloss + cb, lsum);
@@ -250,10 +276,11 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
 template <int K, bool VEC, bool MON>
 __device__ __forceinline__ void window_pass(const EpochArgs& a, uint32_t u, uint32_t j,
                                             uint32_t c0, uint32_t c1, int pass, int lane,
-                                            uint32_t* sh, const double (&uu)[K],
+                                            uint32_t* qbuf, const double (&uu)[K],
                                             double (&acc)[K], double& lsum) {
   const uint64_t r0 = a.rowptr[u];
   const uint32_t cb = a.cbase[u];
+  RowQueue<K, VEC, MON, true> q{qbuf, 0};
   for (uint32_t c = c0; c < c1; ++c) {
     const uint32_t m = __ldcg(a.wcnt + cb + c);
     const uint64_t base = r0 + uint64_t(c) * a.C;
@@ -263,7 +290,7 @@ __device__ __forceinline__ void window_pass(const EpochArgs& a, uint32_t u, uint
       uint32_t pk = 0;
       if (lane < cnt) {
         const uint32_t v = __ldcg(a.wl + base + k0 + lane);
-        uint32_t st = ld_relaxed(a.state + v);
+        const uint32_t st = ld_relaxed(a.state + v);
         const uint32_t age = j - (st >> 1);
         use = pass == 0 ? age > a.R : age <= a.R;
         if (use) {
@@ -271,55 +298,45 @@ __device__ __forceinline__ void window_pass(const EpochArgs& a, uint32_t u, uint
           pk = v | kNewBit;
         }
       }
-      int cu;
-      const uint32_t pkc = compact(sh, lane, use, pk, cu);
-      accumulate_rows<K, VEC, kU, MON, true>(a.fp, pkc, cu, lane, a.d, a.zold, a.znew, uu, acc,
-                                             lsum);
+      q.push(a, lane, use, pk, uu, acc, lsum);
     }
   }
+  q.flush(a, lane, uu, acc, lsum);
 }
 
 template <int K, bool VEC, bool MON>
-__device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint32_t* sh) {
+__device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint32_t* qbuf) {
   using L = Lay<K, VEC>;
   const uint32_t u = a.perm[p];
   const uint32_t j = p / a.b;
   const uint32_t cb = a.cbase[u];
   const uint32_t nch = a.cbase[u + 1] - cb;
   const uint32_t nchL = a.lbase[u + 1] - a.lbase[u];
-  uint32_t f = ld_relaxed(a.vflag + u);
-  while (f == 0) {  // the E work of u (claimed A batches earlier) is not done yet
-    __nanosleep(64);
-    f = ld_relaxed(a.vflag + u);
-  }
-  if (f == 2) {  // finalised by its E item
-    if (nchL == 1) {
-      if (lane == 0) a.vflag[u] = 0;
-    } else if (lane == 0 && atomicAdd(a.lcnt + u, 1u) == nchL - 1) {
-      a.lcnt[u] = 0;
-      a.vflag[u] = 0;
-    }
-    return;
-  }
   float zu[K];
   L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
   double uu[K], acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) { uu[k] = zu[k]; acc[k] = 0.0; }
   double lsum = 0.0;
+  // the E work of u must be complete (its partial and window lists)
+  uint32_t f = ld_relaxed(a.vflag + u);
+  while (f == 0) {
+    __nanosleep(64);
+    f = ld_relaxed(a.vflag + u);
+  }
   const uint32_t c0 = cl * a.G, c1 = umin32(nch, c0 + a.G);
   if (nchL == 1) {  // E total + old window arcs + negatives + recent arcs
     L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
     if (MON) lsum = __ldcg(a.eloss + cb);
-    window_pass<K, VEC, MON>(a, u, j, c0, c1, 0, lane, sh, uu, acc, lsum);
+    window_pass<K, VEC, MON>(a, u, j, c0, c1, 0, lane, qbuf, uu, acc, lsum);
     do_negatives<K, VEC, MON>(a, j, lane, uu, acc, lsum);
-    window_pass<K, VEC, MON>(a, u, j, c0, c1, 1, lane, sh, uu, acc, lsum);
+    window_pass<K, VEC, MON>(a, u, j, c0, c1, 1, lane, qbuf, uu, acc, lsum);
     finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
     if (lane == 0) a.vflag[u] = 0;
     return;
   }
-  window_pass<K, VEC, MON>(a, u, j, c0, c1, 0, lane, sh, uu, acc, lsum);
-  window_pass<K, VEC, MON>(a, u, j, c0, c1, 1, lane, sh, uu, acc, lsum);
+  window_pass<K, VEC, MON>(a, u, j, c0, c1, 0, lane, qbuf, uu, acc, lsum);
+  window_pass<K, VEC, MON>(a, u, j, c0, c1, 1, lane, qbuf, uu, acc, lsum);
   const uint32_t slot = a.lpo[u] + cl;
   L::store_acc(a.lpart + size_t(slot) * a.d, lane, a.d, acc);
   if (MON && lane == 0) __stcg(a.lloss + slot, lsum);
@@ -333,9 +350,9 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   lsum = MON ? __ldcg(a.eloss + cb) : 0.0;
   const uint32_t lp = a.lpo[u];
 #pragma unroll 4
-  for (uint32_t q = 0; q < nchL; ++q) {
-    L::add_acc(a.lpart + size_t(lp + q) * a.d, lane, a.d, acc);
-    if (MON) lsum = __dadd_rn(lsum, __ldcg(a.lloss + lp + q));
+  for (uint32_t qq = 0; qq < nchL; ++qq) {
+    L::add_acc(a.lpart + size_t(lp + qq) * a.d, lane, a.d, acc);
+    if (MON) lsum = __dadd_rn(lsum, __ldcg(a.lloss + lp + qq));
   }
   do_negatives<K, VEC, MON>(a, j, lane, uu, acc, lsum);
   finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
@@ -346,19 +363,24 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
 }
 
 template <int K, bool VEC, bool MON>
-__global__ void __launch_bounds__(256) epoch_kernel(EpochArgs a) {
-  __shared__ uint32_t shc[8][32];
+__global__ void __launch_bounds__(kWarps * 32) epoch_kernel(EpochArgs a) {
+  __shared__ uint32_t qs[kWarps][kQ];
   const int lane = threadIdx.x & 31;
-  uint32_t* sh = shc[threadIdx.x >> 5];
+  const int w = threadIdx.x >> 5;
+  uint32_t* qbuf = qs[w];
+  const bool lrole = w >= kWarps - int(a.lwarps);
+  uint32_t* counter = a.next + (lrole ? 1 : 0);
+  const uint32_t total = lrole ? *a.n_litems : a.n_eitems;
+  const uint2* items = lrole ? a.litems : a.eitems;
   uint32_t it = 0;
-  if (lane == 0) it = atomicAdd(a.next, 1u);
+  if (lane == 0) it = atomicAdd(counter, 1u);
   it = __shfl_sync(kFull, it, 0);
-  while (it < a.nitems) {
+  while (it < total) {
     uint32_t nxt = 0;
-    if (lane == 0) nxt = atomicAdd(a.next, 1u);  // claim ahead: hides the atomic's latency
-    const uint2 item = a.items[it];
-    if (item.y & kLBit) do_L<K, VEC, MON>(a, item.x, item.y & ~kLBit, lane, sh);
-    else do_E<K, VEC, MON>(a, item.x, item.y, lane, sh);
+    if (lane == 0) nxt = atomicAdd(counter, 1u);  // claim ahead: hides the atomic's latency
+    const uint2 item = items[it];
+    if (lrole) do_L<K, VEC, MON>(a, item.x, item.y, lane, qbuf);
+    else do_E<K, VEC, MON>(a, item.x, item.y, lane, qbuf);
     it = __shfl_sync(kFull, nxt, 0);
   }
 }
@@ -366,51 +388,67 @@ __global__ void __launch_bounds__(256) epoch_kernel(EpochArgs a) {
 // ------------------------------------------------------ per-epoch prep
 __global__ void state_kernel(const uint32_t* __restrict__ perm, uint32_t* __restrict__ state,
                              uint32_t n, uint32_t b, const uint32_t* __restrict__ cbase,
-                             const uint32_t* __restrict__ lbase, uint32_t* __restrict__ nE,
-                             uint32_t* __restrict__ nL) {
+                             uint32_t* __restrict__ nE, uint32_t* __restrict__ wtot) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > n) return;
   if (p == n) {
     nE[n] = 0;
-    nL[n] = 0;
     return;
   }
   const uint32_t u = perm[p];
   state[u] = (p / b) << 1;
   nE[p] = cbase[u + 1] - cbase[u];
-  nL[p] = lbase[u + 1] - lbase[u];
+  wtot[u] = 0;
 }
 
-__device__ __forceinline__ uint32_t batch_count(const uint32_t* P, uint32_t t, uint32_t b,
-                                                uint32_t n) {
-  const uint64_t lo = uint64_t(t) * b, hi = umin64(lo + b, n);
-  return P[hi] - P[lo];
+// One warp per chunk: count the window arcs of every vertex (integer atomics).
+__global__ void window_scan_kernel(const uint64_t* __restrict__ rowptr,
+                                   const uint32_t* __restrict__ col,
+                                   const uint32_t* __restrict__ chunk_vertex,
+                                   const uint32_t* __restrict__ cbase,
+                                   const uint32_t* __restrict__ state, uint32_t* __restrict__ wtot,
+                                   uint64_t chunks, uint32_t C, uint32_t W) {
+  const uint64_t cs = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (cs >= chunks) return;
+  const uint32_t u = chunk_vertex[cs];
+  const uint32_t j = state[u] >> 1;
+  if (j == 0) return;  // batch 0 has no earlier batches
+  const uint64_t r0 = rowptr[u], r1 = rowptr[u + 1];
+  const uint64_t e0 = r0 + uint64_t(cs - cbase[u]) * C, e1 = umin64(e0 + C, r1);
+  uint32_t cnt = 0;
+  for (uint64_t e = e0 + lane; e < e1; e += 32) {
+    const uint32_t bv = state[col[e]] >> 1;
+    cnt += (bv < j && bv + W >= j) ? 1u : 0u;
+  }
+#pragma unroll
+  for (int m = 16; m; m >>= 1) cnt += __shfl_xor_sync(kFull, cnt, m);
+  if (lane == 0 && cnt) atomicAdd(wtot + u, cnt);
 }
 
-__global__ void slot_kernel(const uint32_t* __restrict__ EP, const uint32_t* __restrict__ LP,
-                            uint32_t* __restrict__ sz, uint32_t nb, uint32_t A, uint32_t b,
-                            uint32_t n) {
-  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t > nb + A) return;
-  uint32_t v = 0;
-  if (t < nb) v += batch_count(EP, t, b, n);
-  if (t >= A && t - A < nb) v += batch_count(LP, t - A, b, n);
-  sz[t] = v;
+__global__ void needs_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint32_t b,
+                             const uint32_t* __restrict__ wtot, const uint32_t* __restrict__ negwin,
+                             const uint32_t* __restrict__ lbase, uint32_t* __restrict__ needs,
+                             uint32_t* __restrict__ nL) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > n) return;
+  if (p == n) {
+    nL[n] = 0;
+    return;
+  }
+  const uint32_t u = perm[p];
+  const uint32_t nd = (wtot[u] > 0 || negwin[p / b] != 0) ? 1u : 0u;
+  needs[u] = nd;
+  nL[p] = nd ? lbase[u + 1] - lbase[u] : 0u;
 }
 
-__global__ void emit_kernel(const uint32_t* __restrict__ EP, const uint32_t* __restrict__ LP,
-                            const uint32_t* __restrict__ SS, uint2* __restrict__ items,
-                            uint32_t n, uint32_t b, uint32_t nb, uint32_t A) {
+__global__ void emit_kernel(const uint32_t* __restrict__ P, const uint32_t* __restrict__ cnt,
+                            uint2* __restrict__ items, uint32_t n) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
-  const uint32_t j = p / b;
-  const uint64_t j0 = uint64_t(j) * b;
-  const uint32_t eo = SS[j] + (EP[p] - EP[j0]);
-  for (uint32_t c = 0, ne = EP[p + 1] - EP[p]; c < ne; ++c) items[eo + c] = make_uint2(p, c);
-  const uint32_t t = j + A;
-  const uint32_t lo = SS[t] + (t < nb ? batch_count(EP, t, b, n) : 0u) + (LP[p] - LP[j0]);
-  for (uint32_t c = 0, nl = LP[p + 1] - LP[p]; c < nl; ++c)
-    items[lo + c] = make_uint2(p, c | kLBit);
+  const uint32_t o = P[p];
+  for (uint32_t c = 0, m = P[p + 1] - o; c < m; ++c) items[o + c] = make_uint2(p, c);
+  (void)cnt;
 }
 
 __global__ void negs_kernel(uint32_t* __restrict__ out, uint32_t* __restrict__ negwin,
@@ -443,12 +481,13 @@ template <int K, bool VEC, bool MON>
 void launch_epoch_t(Ctx& c, const EpochArgs& a) {
   auto kern = epoch_kernel<K, VEC, MON>;
   int per_sm = 0;
-  F2V_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, 0));
+  F2V_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0));
   if (per_sm < 1) per_sm = 1;
   uint32_t blocks = uint32_t(per_sm) * uint32_t(c.num_sms);
-  const uint32_t need = uint32_t((uint64_t(a.nitems) * 32 + 255) / 256);
+  const uint64_t ew = kWarps - a.lwarps;
+  const uint32_t need = uint32_t(std::max<uint64_t>((a.n_eitems + ew - 1) / ew, 1));
   blocks = std::max(1u, std::min(blocks, need));
-  kern<<<blocks, 256, 0, c.stream>>>(a);
+  kern<<<blocks, kWarps * 32, 0, c.stream>>>(a);
   F2V_CUDA(cudaGetLastError());
   ++c.launches;
 }
@@ -481,15 +520,16 @@ uint32_t env_u32(const char* name, uint32_t dflt) {
 void load_tuning(EpochTuning& t) {
   t.chunk = std::max(1u, env_u32("F2V_CHUNK", t.chunk));
   t.lgroup = std::max(1u, env_u32("F2V_LGROUP", t.lgroup));
-  t.lookahead = std::max(1u, env_u32("F2V_LOOKAHEAD", t.lookahead));
-  t.window = std::max(t.lookahead + 1, env_u32("F2V_WINDOW", t.window));
+  t.window = std::max(1u, env_u32("F2V_WINDOW", t.window));
   t.recent = env_u32("F2V_RECENT", t.recent);
+  t.lwarps = std::min(uint32_t(kWarps - 1), std::max(1u, env_u32("F2V_LWARPS", t.lwarps)));
 }
 
 // Static per-graph chunk / L-group layout (depends on chunk and lgroup only).
 void k_prepare_graph(Ctx& c) {
   const uint32_t C = c.tune.chunk, G = c.tune.lgroup;
   std::vector<uint32_t> cbase(size_t(c.n) + 1), lbase(size_t(c.n) + 1), lpo(c.n ? c.n : 1, 0u);
+  std::vector<uint32_t> cvert;
   uint64_t chunks = 0, lgroups = 0, lslots = 0;
   for (uint32_t u = 0; u < c.n; ++u) {
     const uint64_t deg = c.h_rowptr[u + 1] - c.h_rowptr[u];
@@ -508,6 +548,9 @@ void k_prepare_graph(Ctx& c) {
   }
   cbase[c.n] = uint32_t(chunks);
   lbase[c.n] = uint32_t(lgroups);
+  cvert.resize(std::max<uint64_t>(chunks, 1));
+  for (uint32_t u = 0; u < c.n; ++u)
+    for (uint32_t q = cbase[u]; q < cbase[u + 1]; ++q) cvert[q] = u;
   c.chunks = chunks;
   c.lgroups = lgroups;
   c.lslots = lslots;
@@ -516,12 +559,15 @@ void k_prepare_graph(Ctx& c) {
   c.cbase.ensure(sizeof(uint32_t) * (size_t(c.n) + 1));
   c.lbase.ensure(sizeof(uint32_t) * (size_t(c.n) + 1));
   c.lpo.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
+  c.cvert.ensure(sizeof(uint32_t) * cvert.size());
   c.ecnt.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
   c.lcnt.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
   c.vflag.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
   F2V_CUDA(cudaMemcpyAsync(c.cbase.p, cbase.data(), sizeof(uint32_t) * (c.n + 1),
                            cudaMemcpyHostToDevice, c.stream));
   F2V_CUDA(cudaMemcpyAsync(c.lbase.p, lbase.data(), sizeof(uint32_t) * (c.n + 1),
+                           cudaMemcpyHostToDevice, c.stream));
+  F2V_CUDA(cudaMemcpyAsync(c.cvert.p, cvert.data(), sizeof(uint32_t) * cvert.size(),
                            cudaMemcpyHostToDevice, c.stream));
   if (c.n) {
     F2V_CUDA(cudaMemcpyAsync(c.lpo.p, lpo.data(), sizeof(uint32_t) * c.n,
@@ -533,12 +579,11 @@ void k_prepare_graph(Ctx& c) {
   F2V_CUDA(cudaStreamSynchronize(c.stream));
 }
 
-// Per-epoch preparation: perm (already in c.perm) -> state, the ordered work
-// items, the negatives of every batch and their window flags.
+// Per-epoch preparation: perm (already in c.perm) -> state, the negatives of
+// every batch + window flags, the window pre-scan, the two ordered item lists.
 void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed, int sampler) {
   const uint32_t n = c.n;
   const uint32_t nb = uint32_t((uint64_t(n) + b - 1) / b);
-  const uint32_t A = c.tune.lookahead;
   if (c.prepared_chunk != c.tune.chunk || c.prepared_lgroup != c.tune.lgroup)
     k_prepare_graph(c);
   c.state.ensure(sizeof(uint32_t) * n);
@@ -546,9 +591,10 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
   c.nL.ensure(sizeof(uint32_t) * (n + 1));
   c.EP.ensure(sizeof(uint32_t) * (n + 1));
   c.LP.ensure(sizeof(uint32_t) * (n + 1));
-  c.sz.ensure(sizeof(uint32_t) * (size_t(nb) + A + 1));
-  c.SS.ensure(sizeof(uint32_t) * (size_t(nb) + A + 1));
-  c.items.ensure(sizeof(uint2) * std::max<uint64_t>(c.chunks + c.lgroups, 1));
+  c.wtot.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  c.needs.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  c.items.ensure(sizeof(uint2) * std::max<uint64_t>(c.chunks, 1));
+  c.litems.ensure(sizeof(uint2) * std::max<uint64_t>(c.lgroups, 1));
   c.negs_all.ensure(sizeof(uint32_t) * std::max<uint64_t>(uint64_t(nb) * s, 1));
   c.negwin.ensure(sizeof(uint32_t) * std::max<uint32_t>(nb, 1));
   c.epart.ensure(sizeof(double) * std::max<uint64_t>(c.chunks * c.d, 1));
@@ -559,41 +605,50 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
   c.lloss.ensure(sizeof(double) * std::max<uint64_t>(c.lslots, 1));
   c.ploss.ensure(sizeof(double) * std::max<uint32_t>(n, 1));
   c.counters.ensure(64);
-  state_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
-      c.perm.as<uint32_t>(), c.state.as<uint32_t>(), n, b, c.cbase.as<uint32_t>(),
-      c.lbase.as<uint32_t>(), c.nE.as<uint32_t>(), c.nL.as<uint32_t>());
+  const uint32_t W = c.tune.window;
+  state_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(c.perm.as<uint32_t>(),
+                                                         c.state.as<uint32_t>(), n, b,
+                                                         c.cbase.as<uint32_t>(),
+                                                         c.nE.as<uint32_t>(), c.wtot.as<uint32_t>());
   F2V_CUDA(cudaGetLastError());
-  size_t tmp = 0, tmp2 = 0;
+  negs_kernel<<<(nb + 255) / 256, 256, 0, c.stream>>>(
+      c.negs_all.as<uint32_t>(), c.negwin.as<uint32_t>(), c.state.as<uint32_t>(), nb, s, n, seed,
+      epoch, sampler, W);
+  F2V_CUDA(cudaGetLastError());
+  window_scan_kernel<<<uint32_t((c.chunks * 32 + 255) / 256), 256, 0, c.stream>>>(
+      c.rowptr.as<uint64_t>(), c.col.as<uint32_t>(), c.cvert.as<uint32_t>(),
+      c.cbase.as<uint32_t>(), c.state.as<uint32_t>(), c.wtot.as<uint32_t>(), c.chunks,
+      c.tune.chunk, W);
+  F2V_CUDA(cudaGetLastError());
+  needs_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
+      c.perm.as<uint32_t>(), n, b, c.wtot.as<uint32_t>(), c.negwin.as<uint32_t>(),
+      c.lbase.as<uint32_t>(), c.needs.as<uint32_t>(), c.nL.as<uint32_t>());
+  F2V_CUDA(cudaGetLastError());
+  size_t tmp = 0;
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.nE.as<uint32_t>(), c.EP.as<uint32_t>(),
                                          n + 1, c.stream));
-  F2V_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp2, c.sz.as<uint32_t>(),
-                                         c.SS.as<uint32_t>(), nb + A + 1, c.stream));
-  c.scan_tmp.ensure(std::max(tmp, tmp2));
+  c.scan_tmp.ensure(tmp);
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.nE.as<uint32_t>(),
                                          c.EP.as<uint32_t>(), n + 1, c.stream));
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.nL.as<uint32_t>(),
                                          c.LP.as<uint32_t>(), n + 1, c.stream));
-  slot_kernel<<<(nb + A + 1 + 255) / 256, 256, 0, c.stream>>>(
-      c.EP.as<uint32_t>(), c.LP.as<uint32_t>(), c.sz.as<uint32_t>(), nb, A, b, n);
+  emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.EP.as<uint32_t>(), c.nE.as<uint32_t>(),
+                                                     c.items.as<uint2>(), n);
   F2V_CUDA(cudaGetLastError());
-  F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp2, c.sz.as<uint32_t>(),
-                                         c.SS.as<uint32_t>(), nb + A + 1, c.stream));
-  emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.EP.as<uint32_t>(), c.LP.as<uint32_t>(),
-                                                     c.SS.as<uint32_t>(), c.items.as<uint2>(), n,
-                                                     b, nb, A);
+  emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.LP.as<uint32_t>(), c.nL.as<uint32_t>(),
+                                                     c.litems.as<uint2>(), n);
   F2V_CUDA(cudaGetLastError());
-  negs_kernel<<<(nb + 255) / 256, 256, 0, c.stream>>>(
-      c.negs_all.as<uint32_t>(), c.negwin.as<uint32_t>(), c.state.as<uint32_t>(), nb, s, n, seed,
-      epoch, sampler, c.tune.window);
-  F2V_CUDA(cudaGetLastError());
-  c.launches += 8;
+  // number of L items (device value, read back asynchronously with the run)
+  F2V_CUDA(cudaMemcpyAsync(c.counters.as<uint32_t>() + 8, c.LP.as<uint32_t>() + n,
+                           sizeof(uint32_t), cudaMemcpyDeviceToDevice, c.stream));
+  c.launches += 9;
 }
 
 EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForceParams& fp,
                         bool monitor) {
   const int nxt = 1 - c.cur;
   c.z[nxt].ensure(sizeof(float) * size_t(c.n) * c.d);
-  uint32_t* ctr = c.counters.as<uint32_t>();  // [0] next item, [2..3] bad (u64), [4..5] loss
+  uint32_t* ctr = c.counters.as<uint32_t>();  // [0..1] claims, [2..3] bad, [4..5] loss, [8] nL
   F2V_CUDA(cudaMemsetAsync(ctr, 0, 8, c.stream));
   F2V_CUDA(cudaMemsetAsync(ctr + 2, 0xff, 8, c.stream));
   EpochArgs a;
@@ -605,12 +660,15 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.state = c.state.as<uint32_t>();
   a.negs = c.negs_all.as<uint32_t>();
   a.negwin = c.negwin.as<uint32_t>();
-  a.items = c.items.as<uint2>();
-  a.nitems = uint32_t(c.chunks + c.lgroups);
+  a.eitems = c.items.as<uint2>();
+  a.litems = c.litems.as<uint2>();
+  a.n_eitems = uint32_t(c.chunks);
+  a.n_litems = ctr + 8;
   a.next = ctr;
   a.cbase = c.cbase.as<uint32_t>();
   a.lbase = c.lbase.as<uint32_t>();
   a.lpo = c.lpo.as<uint32_t>();
+  a.needs = c.needs.as<uint32_t>();
   a.epart = c.epart.as<double>();
   a.eloss = c.eloss.as<double>();
   a.wcnt = c.wcnt.as<uint32_t>();
@@ -628,9 +686,9 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.s = s;
   a.C = c.tune.chunk;
   a.G = c.tune.lgroup;
-  a.A = c.tune.lookahead;
   a.W = c.tune.window;
   a.R = c.tune.recent;
+  a.lwarps = c.tune.lwarps;
   a.eta = eta;
   a.fp = fp;
   if (!c.ev_kernel.size()) {
@@ -648,13 +706,14 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
     F2V_CUDA(cudaGetLastError());
     ++c.launches;
   }
-  uint64_t host[3];
-  F2V_CUDA(cudaMemcpyAsync(host, ctr, 24, cudaMemcpyDeviceToHost, c.stream));
+  uint64_t host[5];
+  F2V_CUDA(cudaMemcpyAsync(host, ctr, 40, cudaMemcpyDeviceToHost, c.stream));
   F2V_CUDA(cudaStreamSynchronize(c.stream));
   float kms = 0.f;
   F2V_CUDA(cudaEventElapsedTime(&kms, c.ev_kernel[0], c.ev_kernel[1]));
   c.timing[1] += kms;
   c.timing[2] += 1;
+  c.last_litems = uint32_t(host[4]);
   EpochResult r{host[1], 0.0};
   if (monitor) std::memcpy(&r.loss, &host[2], sizeof(double));
   c.cur = nxt;  // Znew becomes the current embedding

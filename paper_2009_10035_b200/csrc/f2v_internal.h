@@ -40,11 +40,11 @@ struct DeviceBuf {
 // Tunables of the dataflow epoch kernel; each can
 // be overridden by the environment variable named beside it.
 struct EpochTuning {
-  uint32_t chunk = 256;     // F2V_CHUNK: max arcs per E item (hub splitting)
-  uint32_t lgroup = 8;      // F2V_LGROUP: E chunks per L item
-  uint32_t lookahead = 32;  // F2V_LOOKAHEAD: E items run this many batches ahead
-  uint32_t window = 48;     // F2V_WINDOW: arcs to batches [j-window, j) wait for L
-  uint32_t recent = 2;      // F2V_RECENT: window arcs this recent are taken last
+  uint32_t chunk = 256;  // F2V_CHUNK: max arcs per E item (hub splitting)
+  uint32_t lgroup = 8;   // F2V_LGROUP: E chunks per L item
+  uint32_t window = 48;  // F2V_WINDOW: arcs to batches [j-window, j) go to L items
+  uint32_t recent = 2;   // F2V_RECENT: window arcs this recent are taken last
+  uint32_t lwarps = 2;   // F2V_LWARPS: L-role warps per 8-warp CTA
 };
 void load_tuning(EpochTuning& t);
 
@@ -62,7 +62,7 @@ struct Ctx {
   DeviceBuf rowptr, col;
   std::vector<uint64_t> h_rowptr;  // host copy: degrees for counters/partials
   // chunk / L-group layout, static per (graph, chunk, lgroup)
-  DeviceBuf cbase, lbase, lpo, ecnt, lcnt, vflag;
+  DeviceBuf cbase, lbase, lpo, cvert, ecnt, lcnt, vflag;
   uint64_t chunks = 0, lgroups = 0, lslots = 0;
   uint32_t prepared_chunk = 0, prepared_lgroup = 0;
 
@@ -76,8 +76,9 @@ struct Ctx {
   uint32_t staged_b = 0;
 
   // epoch buffers
-  DeviceBuf perm, state, negs_all, negwin, items, nE, nL, EP, LP, sz, SS, scan_tmp, epart, eloss,
-      wcnt, wl, lpart, lloss, ploss, counters;
+  DeviceBuf perm, state, negs_all, negwin, items, litems, nE, nL, EP, LP, wtot, needs, scan_tmp,
+      epart, eloss, wcnt, wl, lpart, lloss, ploss, counters;
+  uint32_t last_litems = 0;
 
   // timing of the last train_epochs call (f2v_last_timing)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
