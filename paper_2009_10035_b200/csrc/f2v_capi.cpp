@@ -269,7 +269,7 @@ void f2v_destroy(f2v_ctx* h) {
         &c.z[0], &c.z[1], &c.grads, &c.ids, &c.negs, &c.vloss, &c.bad, &c.scratch, &c.perm,
         &c.state, &c.negs_all, &c.negwin, &c.items, &c.litems, &c.nE, &c.nL, &c.EP, &c.LP,
         &c.wtot, &c.needs, &c.scan_tmp, &c.epart, &c.eloss, &c.wcnt, &c.wl, &c.lpart, &c.lloss,
-        &c.ploss, &c.counters})
+        &c.ploss, &c.counters, &c.trace})
     b->release();
   for (cudaEvent_t e : c.ev_kernel) cudaEventDestroy(e);
   if (c.ev_begin) cudaEventDestroy(c.ev_begin);
@@ -279,6 +279,17 @@ void f2v_destroy(f2v_ctx* h) {
 }
 
 const char* f2v_last_error(const f2v_ctx* h) { return h ? h->c.err.c_str() : ""; }
+
+// DEBUG helper (not in the public header): per-position finalise timestamps
+// of the last epoch (F2V_TRACE) and the L-item count.
+int32_t f2v_debug_trace(f2v_ctx* h, uint64_t* out, uint32_t* litems) {
+  if (!h || !h->c.trace.p) return F2V_EUSAGE;
+  if (litems) *litems = h->c.last_litems;
+  return cudaMemcpy(out, h->c.trace.p, sizeof(uint64_t) * h->c.n, cudaMemcpyDeviceToHost) ==
+                 cudaSuccess
+             ? F2V_OK
+             : F2V_ECUDA;
+}
 
 int32_t f2v_last_timing(const f2v_ctx* h, double* out4) {
   if (!h) return F2V_EUSAGE;

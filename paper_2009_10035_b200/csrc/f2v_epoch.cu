@@ -83,7 +83,15 @@ struct EpochArgs {
   uint32_t C, G, W, R, lwarps;
   float eta;
   ForceParams fp;
+  int nodep;                    // DEBUG (F2V_DEBUG_NODEP): every row read from Zold, no waits
+  unsigned long long* trace;    // DEBUG (F2V_TRACE): per position finalise time (ns)
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t wait_written(const uint32_t* state, uint32_t v, uint32_t st) {
   while (!(st & 1u)) {
@@ -141,7 +149,7 @@ __device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, int
     if (lane < cnt) {
       const uint32_t w = a.negs[size_t(j) * a.s + k0 + lane];
       const uint32_t st = ld_relaxed(a.state + w);
-      if ((st >> 1) < j) {
+      if ((st >> 1) < j && !a.nodep) {
         wait_written(a.state, w, st);
         pk = w | kNewBit;
       } else {
@@ -176,6 +184,7 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_
   if (lane == 0) {
     if (any_bad) atomicMin(a.bad, (unsigned long long)p);
     atomicOr(a.state + u, 1u);
+    if (a.trace) a.trace[p] = globaltimer();
   }
 }
 
@@ -206,7 +215,7 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
       v = a.col[e + lane];
       const uint32_t st = ld_relaxed(a.state + v);
       const uint32_t bv = st >> 1;
-      if (bv >= j) {
+      if (bv >= j || a.nodep) {
         use = true;
         pk = v;
       } else if (bv + a.W < j) {  // past: final long ago (rarely waits)
@@ -429,7 +438,7 @@ __global__ void window_scan_kernel(const uint64_t* __restrict__ rowptr,
 __global__ void needs_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint32_t b,
                              const uint32_t* __restrict__ wtot, const uint32_t* __restrict__ negwin,
                              const uint32_t* __restrict__ lbase, uint32_t* __restrict__ needs,
-                             uint32_t* __restrict__ nL) {
+                             uint32_t* __restrict__ nL, int nodep) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > n) return;
   if (p == n) {
@@ -437,7 +446,7 @@ __global__ void needs_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint
     return;
   }
   const uint32_t u = perm[p];
-  const uint32_t nd = (wtot[u] > 0 || negwin[p / b] != 0) ? 1u : 0u;
+  const uint32_t nd = (wtot[u] > 0 || negwin[p / b] != 0) && !nodep ? 1u : 0u;
   needs[u] = nd;
   nL[p] = nd ? lbase[u + 1] - lbase[u] : 0u;
 }
@@ -622,7 +631,8 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
   F2V_CUDA(cudaGetLastError());
   needs_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
       c.perm.as<uint32_t>(), n, b, c.wtot.as<uint32_t>(), c.negwin.as<uint32_t>(),
-      c.lbase.as<uint32_t>(), c.needs.as<uint32_t>(), c.nL.as<uint32_t>());
+      c.lbase.as<uint32_t>(), c.needs.as<uint32_t>(), c.nL.as<uint32_t>(),
+      std::getenv("F2V_DEBUG_NODEP") ? 1 : 0);
   F2V_CUDA(cudaGetLastError());
   size_t tmp = 0;
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.nE.as<uint32_t>(), c.EP.as<uint32_t>(),
@@ -691,6 +701,12 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.lwarps = c.tune.lwarps;
   a.eta = eta;
   a.fp = fp;
+  a.nodep = std::getenv("F2V_DEBUG_NODEP") ? 1 : 0;
+  a.trace = nullptr;
+  if (std::getenv("F2V_TRACE")) {
+    c.trace.ensure(sizeof(unsigned long long) * std::max<uint32_t>(c.n, 1));
+    a.trace = c.trace.as<unsigned long long>();
+  }
   if (!c.ev_kernel.size()) {
     c.ev_kernel.resize(2);
     F2V_CUDA(cudaEventCreate(&c.ev_kernel[0]));

@@ -79,6 +79,7 @@ struct Ctx {
   DeviceBuf perm, state, negs_all, negwin, items, litems, nE, nL, EP, LP, wtot, needs, scan_tmp,
       epart, eloss, wcnt, wl, lpart, lloss, ploss, counters;
   uint32_t last_litems = 0;
+  DeviceBuf trace;  // DEBUG: per-position finalise timestamps (F2V_TRACE)
 
   // timing of the last train_epochs call (f2v_last_timing)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;

@@ -6,10 +6,28 @@ import io
 import subprocess
 import sys
 
+import gzip
+import os
+
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-raw = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
-                     text=True).stdout
+
+
+def page(name, *extra):
+    """From a .ncu-rep, or from the CSVs profiles/ncu_export.sh wrote (prefix)."""
+    if rep.endswith(".ncu-rep"):
+        return subprocess.run(["ncu", "-i", rep, "--page", name, "--csv", *extra],
+                              capture_output=True, text=True).stdout
+    key = {"details": "details.csv", "raw": "raw.csv"}.get(name)
+    if key is None:
+        key = "cudasass.csv.gz" if "cuda,sass" in extra else "sass.csv.gz"
+    path = f"{rep}.{key}"
+    if path.endswith(".gz"):
+        return gzip.open(path, "rt").read()
+    return open(path).read()
+
+
+raw = page("details")
 rows = list(csv.reader(io.StringIO(raw)))
 hdr = rows[0]
 want = ["Duration", "DRAM Throughput", "Memory Throughput", "L2 Hit Rate", "Executed Ipc Active",
@@ -20,7 +38,7 @@ for r in rows[1:]:
     d = dict(zip(hdr, r))
     if d.get("Metric Name") in want:
         print(f"{d['Metric Name']:40s} {d['Metric Value']} {d['Metric Unit']}")
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+raw = page("raw")
 rows = list(csv.reader(io.StringIO(raw)))
 h, units, vals = rows[0], rows[1], rows[2]
 for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
@@ -33,8 +51,7 @@ for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_bytes.sum",
     if k in h:
         i = h.index(k)
         print(f"{k:60s} {vals[i]} {units[i]}")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+src = page("source", "--print-source", "sass")
 rows = list(csv.reader(io.StringIO(src)))
 hdr = rows[1]
 data = rows[2:]
@@ -49,3 +66,31 @@ for k, v in sorted(agg.items(), key=lambda x: -x[1])[:8]:
 for r in sorted(data, key=lambda r: -int(r[ix[S]] or 0))[:top]:
     print(f"{int(r[ix[S]] or 0) * 100 / max(tot, 1):5.1f}% exec={r[ix['Instructions Executed']]:>12s}  "
           f"{r[ix['Source']][:80]}")
+
+# per source line (cuda,sass view)
+try:
+    src = page("source", "--print-source", "cuda,sass")
+    rows = list(csv.reader(io.StringIO(src)))
+    cur, line, agg = None, None, {}
+    for r in rows:
+        if not r:
+            continue
+        if r[0] == "File Path":
+            cur = r[1].split("/")[-1]
+            continue
+        if r[0] in ("Function Name", "Line No"):
+            continue
+        if r[0]:
+            line = (cur, r[0], r[1][:80])
+            continue
+        try:
+            s_ = int(r[4] or 0)
+        except (ValueError, IndexError):
+            continue
+        agg[line] = agg.get(line, 0) + s_
+    tot = max(sum(agg.values()), 1)
+    print("--- hottest source lines")
+    for k, v in sorted(agg.items(), key=lambda x: -x[1])[:top]:
+        print(f"{100 * v / tot:5.1f}% {k[0]}:{k[1]} {k[2]}")
+except Exception as ex:  # noqa
+    print("no cuda,sass view:", ex)
