@@ -46,6 +46,12 @@ extern "C" {
 #define F2V_SAMPLER_SPLITMIX 0 /* the reference's Rng::keyed(seed,{0x33,epoch,batch}) */
 #define F2V_SAMPLER_PHILOX 1   /* Philox4x32-10 keyed by seed, counter (k,batch,epoch,shard) */
 
+/* pair-math precision of the device epochs:
+ * FAST  = fp32 dot/distance/force term, fp64 accumulation (~1e-7 of the reference);
+ * EXACT = fp64 everything in the reference's operation order (bitwise in practice). */
+#define F2V_PRECISION_FAST 0
+#define F2V_PRECISION_EXACT 1
+
 /* ForceModel, force_kernels.hpp:17-21 */
 typedef struct {
   int32_t kind;          /* F2V_SIGMOID .. F2V_LINLOG */
@@ -68,6 +74,7 @@ typedef struct {
   int32_t init;          /* 0: caller's Z; 1: init_embedding (trainer.cpp:62-72) */
   uint32_t first_epoch;  /* run epochs [first_epoch, first_epoch + run_epochs) of the */
   uint32_t run_epochs;   /* `epochs`-long schedule; run_epochs 0 = through the end */
+  int32_t precision;     /* F2V_PRECISION_FAST (default) or F2V_PRECISION_EXACT */
 } f2v_train_config;
 
 /* TrainCounters, trainer.hpp:83-87 */

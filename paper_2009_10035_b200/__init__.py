@@ -81,7 +81,7 @@ class _TrainConfig(C.Structure):
                 ("lr", C.c_float), ("epochs", C.c_uint32), ("model", _ForceModel),
                 ("seed", C.c_uint64), ("lr_decay", C.c_int32), ("monitor_loss", C.c_int32),
                 ("sampler", C.c_int32), ("init", C.c_int32), ("first_epoch", C.c_uint32),
-                ("run_epochs", C.c_uint32)]
+                ("run_epochs", C.c_uint32), ("precision", C.c_int32)]
 
 
 class _Counters(C.Structure):
@@ -217,6 +217,7 @@ class TrainConfig:
     lr_decay: str = "constant"  # or "linear_to_zero"
     monitor_loss: bool = False
     sampler: str = "splitmix"
+    precision: str = "fast"  # "fast" (fp32 pair math, fp64 accumulate) or "exact" (fp64)
 
     def _c(self, init: int = 0, first_epoch: int = 0, run_epochs: int = 0) -> _TrainConfig:
         if self.lr_decay not in ("constant", "linear_to_zero"):
@@ -225,10 +226,13 @@ class TrainConfig:
             raise UsageError(f"unknown sampler {self.sampler}")
         if self.workers < 1:
             raise UsageError("workers must be >= 1")
+        if self.precision not in ("fast", "exact"):
+            raise UsageError("precision must be fast or exact")
         return _TrainConfig(self.dim, self.batch, self.negatives, self.lr, self.epochs,
                             self.model._c(), self.seed & (2**64 - 1),
                             int(self.lr_decay == "linear_to_zero"), int(self.monitor_loss),
-                            SAMPLERS[self.sampler], init, first_epoch, run_epochs)
+                            SAMPLERS[self.sampler], init, first_epoch, run_epochs,
+                            0 if self.precision == "fast" else 1)
 
 
 @dataclasses.dataclass

@@ -45,16 +45,22 @@ def build(verbose: bool = False, force: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    objs = []
     tmpdir = os.path.join(LIBDIR, "obj")
     os.makedirs(tmpdir, exist_ok=True)
+    jobs = []
     for src in sources():
         obj = os.path.join(tmpdir, os.path.basename(src) + ".o")
         cmd = ["nvcc", *NVCC_FLAGS, "-c", src, "-o", obj]
         if verbose and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
-        subprocess.check_call(cmd)
-        objs.append(obj)
+        jobs.append((cmd, obj))
+    # translation units compile in parallel (the epoch kernel has many
+    # instantiations split across files)
+    procs = [(subprocess.Popen(cmd), obj) for cmd, obj in jobs]
+    for p, obj in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, "nvcc " + obj)
+    objs = [obj for _, obj in procs]
     cmd = ["nvcc", *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-Xcompiler", "-pthread"]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)

@@ -162,6 +162,10 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
   if (cfg.sampler != F2V_SAMPLER_SPLITMIX && cfg.sampler != F2V_SAMPLER_PHILOX)
     fail(F2V_EUSAGE, "unknown sampler");
   if (c.n >= 0x80000000u) fail(F2V_EUSAGE, "n must be < 2^31");
+  if (cfg.precision != F2V_PRECISION_FAST && cfg.precision != F2V_PRECISION_EXACT)
+    fail(F2V_EUSAGE, "unknown precision");
+  const char* penv = std::getenv("F2V_PRECISION");  // test/debug override
+  c.tune.fast = penv ? (std::strcmp(penv, "exact") != 0) : cfg.precision == F2V_PRECISION_FAST;
   if (cfg.init == 1) {
     c.d = cfg.dim;
     c.cur = 0;

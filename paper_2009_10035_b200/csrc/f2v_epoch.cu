@@ -34,9 +34,7 @@
 #include <cstring>
 #include <vector>
 
-#include "f2v_internal.h"
-#include "f2v_pair.cuh"
-#include "f2v_rng.h"
+#include "f2v_epoch.cuh"
 
 namespace f2v {
 
@@ -45,354 +43,6 @@ __global__ void sum_kernel(const double* __restrict__ v, uint64_t m, double* out
 namespace {
 
 using namespace dev;
-
-constexpr int kU = 4;           // rows in flight per warp per accumulate step
-constexpr int kWarps = 8;       // warps per CTA
-constexpr int kQ = 64;          // per-warp compaction queue (entries)
-
-struct EpochArgs {
-  const uint64_t* rowptr;
-  const uint32_t* col;
-  const float* zold;
-  float* znew;
-  const uint32_t* perm;
-  uint32_t* state;
-  const uint32_t* negs;
-  const uint32_t* negwin;
-  const uint2* eitems;
-  const uint2* litems;
-  uint32_t n_eitems;
-  const uint32_t* n_litems;  // device count (written by the prep)
-  uint32_t* next;  // [0] E claims, [1] L claims
-  const uint32_t* cbase;
-  const uint32_t* lbase;
-  const uint32_t* lpo;
-  const uint32_t* needs;  // per vertex: window arcs/negatives exist
-  double* epart;
-  double* eloss;
-  uint32_t* wcnt;
-  uint32_t* wl;
-  double* lpart;
-  double* lloss;
-  uint32_t* ecnt;
-  uint32_t* lcnt;
-  uint32_t* vflag;
-  double* ploss;
-  unsigned long long* bad;
-  uint32_t n, d, b, s;
-  uint32_t C, G, W, R, lwarps;
-  float eta;
-  ForceParams fp;
-  int nodep;                    // DEBUG (F2V_DEBUG_NODEP): every row read from Zold, no waits
-  unsigned long long* trace;    // DEBUG (F2V_TRACE): per position finalise time (ns)
-};
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-
-__device__ __forceinline__ uint32_t wait_written(const uint32_t* state, uint32_t v, uint32_t st) {
-  while (!(st & 1u)) {
-    __nanosleep(32);
-    st = ld_relaxed(state + v);
-  }
-  return st;
-}
-
-__device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
-
-// Per-warp FIFO of packed row ids (bit 31 = Znew) in shared memory; rows
-// are accumulated 32 at a time in push order (= the deterministic pair order).
-template <int K, bool VEC, bool MON, bool ATT>
-struct RowQueue {
-  uint32_t* buf;
-  int n;
-  __device__ __forceinline__ void push(const EpochArgs& a, int lane, bool keep, uint32_t val,
-                                       const double (&uu)[K], double (&acc)[K], double& lsum) {
-    const uint32_t m = __ballot_sync(kFull, keep);
-    if (keep) buf[n + __popc(m & lanemask_lt(lane))] = val;
-    __syncwarp();
-    n += __popc(m);
-    if (n >= 32) {
-      const uint32_t pk = buf[lane];
-      const uint32_t rest = lane + 32 < n ? buf[lane + 32] : 0u;
-      __syncwarp();
-      buf[lane] = rest;
-      __syncwarp();
-      n -= 32;
-      accumulate_rows<K, VEC, kU, MON, ATT>(a.fp, pk, 32, lane, a.d, a.zold, a.znew, uu, acc,
-                                            lsum);
-    }
-  }
-  __device__ __forceinline__ void flush(const EpochArgs& a, int lane, const double (&uu)[K],
-                                        double (&acc)[K], double& lsum) {
-    if (n == 0) return;
-    const uint32_t pk = lane < n ? buf[lane] : 0u;
-    __syncwarp();
-    const int cnt = n;
-    n = 0;
-    accumulate_rows<K, VEC, kU, MON, ATT>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew, uu, acc,
-                                          lsum);
-  }
-};
-
-// The shared negatives of batch j, in sample order (sampling.cpp:59).
-template <int K, bool VEC, bool MON>
-__device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, int lane,
-                                             const double (&uu)[K], double (&acc)[K],
-                                             double& lsum) {
-  for (uint32_t k0 = 0; k0 < a.s; k0 += 32) {
-    const int cnt = int(umin32(32, a.s - k0));
-    uint32_t pk = 0;
-    if (lane < cnt) {
-      const uint32_t w = a.negs[size_t(j) * a.s + k0 + lane];
-      const uint32_t st = ld_relaxed(a.state + w);
-      if ((st >> 1) < j && !a.nodep) {
-        wait_written(a.state, w, st);
-        pk = w | kNewBit;
-      } else {
-        pk = w;
-      }
-    }
-    accumulate_rows<K, VEC, kU, MON, false>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew, uu, acc,
-                                            lsum);
-  }
-}
-
-// g = float(acc) (trainer.cpp:140-145); z_u -= eta*g in fp32 (trainer.cpp:173);
-// publish row u of Znew.
-template <int K, bool VEC, bool MON>
-__device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_t u, int lane,
-                                         const float (&zu)[K], const double (&acc)[K],
-                                         double lsum) {
-  using L = Lay<K, VEC>;
-  bool bad = false;
-  float nz[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    const float g = __double2float_rn(acc[k]);
-    if (L::valid(lane, k, a.d) && !isfinite(g)) bad = true;
-    nz[k] = __fsub_rn(zu[k], __fmul_rn(a.eta, g));
-  }
-  L::store(a.znew + size_t(u) * a.d, lane, a.d, nz);
-  const bool any_bad = __any_sync(kFull, bad);
-  if (MON && lane == 0) a.ploss[p] = lsum;
-  __threadfence();
-  __syncwarp();
-  if (lane == 0) {
-    if (any_bad) atomicMin(a.bad, (unsigned long long)p);
-    atomicOr(a.state + u, 1u);
-    if (a.trace) a.trace[p] = globaltimer();
-  }
-}
-
-template <int K, bool VEC, bool MON>
-__device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint32_t* qbuf) {
-  using L = Lay<K, VEC>;
-  const uint32_t u = a.perm[p];
-  const uint32_t j = p / a.b;
-  const uint64_t r0 = a.rowptr[u], r1 = a.rowptr[u + 1];
-  const uint32_t cb = a.cbase[u];
-  const uint32_t nch = a.cbase[u + 1] - cb;
-  const uint32_t cs = cb + c;
-  const uint64_t e0 = r0 + uint64_t(c) * a.C;
-  const uint64_t e1 = umin64(e0 + a.C, r1);
-  float zu[K];
-  L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
-  double uu[K], acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) { uu[k] = zu[k]; acc[k] = 0.0; }
-  double lsum = 0.0;
-  uint32_t wc = 0;
-  RowQueue<K, VEC, MON, true> q{qbuf, 0};
-  for (uint64_t e = e0; e < e1; e += 32) {
-    const int cnt = int(umin64(32, e1 - e));
-    uint32_t v = 0, pk = 0;
-    bool use = false, win = false;
-    if (lane < cnt) {
-      v = a.col[e + lane];
-      const uint32_t st = ld_relaxed(a.state + v);
-      const uint32_t bv = st >> 1;
-      if (bv >= j || a.nodep) {
-        use = true;
-        pk = v;
-      } else if (bv + a.W < j) {  // past: final long ago (rarely waits)
-        wait_written(a.state, v, st);
-        use = true;
-        pk = v | kNewBit;
-      } else {
-        win = true;
-      }
-    }
-    const uint32_t wm = __ballot_sync(kFull, win);
-    if (win) a.wl[e0 + wc + __popc(wm & lanemask_lt(lane))] = v;
-    wc += __popc(wm);
-    q.push(a, lane, use, pk, uu, acc, lsum);
-  }
-  q.flush(a, lane, uu, acc, lsum);
-  const bool needs = a.needs[u] != 0;
-  if (nch == 1) {
-    if (!needs) {
-      do_negatives<K, VEC, MON>(a, j, lane, uu, acc, lsum);
-      finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
-    } else {
-      L::store_acc(a.epart + size_t(cs) * a.d, lane, a.d, acc);
-      if (lane == 0) {
-        if (MON) __stcg(a.eloss + cs, lsum);
-        __stcg(a.wcnt + cs, wc);
-      }
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) st_relaxed(a.vflag + u, 1u);
-    }
-    return;
-  }
-  // hub chunk: publish the partial; the last E arrival combines in chunk order
-  L::store_acc(a.epart + size_t(cs) * a.d, lane, a.d, acc);
-  if (lane == 0) {
-    if (MON) __stcg(a.eloss + cs, lsum);
-    __stcg(a.wcnt + cs, wc);
-  }
-  __threadfence();
-  __syncwarp();
-  uint32_t last = 0;
-  if (lane == 0) last = atomicAdd(a.ecnt + u, 1u) == nch - 1 ? 1u : 0u;
-  if (!__shfl_sync(kFull, last, 0)) return;
-  __threadfence();
-  L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
-  lsum = MON ? __ldcg(a.eloss + cb) : 0.0;
-#pragma unroll 4
-  for (uint32_t qq = 1; qq < nch; ++qq) {
-    L::add_acc(a.epart + size_t(cb + qq) * a.d, lane, a.d, acc);
-    if (MON) lsum = __dadd_rn(lsum, __ldcg(a.eloss + cb + qq));
-  }
-  if (lane == 0) a.ecnt[u] = 0;
-  if (!needs) {
-    do_negatives<K, VEC, MON>(a, j, lane, uu, acc, lsum);
-    finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
-  } else {
-    L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);  // the E total
-    if (MON && lane == 0) __stcg(a.eloss + cb, lsum);
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_relaxed(a.vflag + u, 1u);
-  }
-}
-
-// Window arcs of chunks [c0, c1) of u: pass 0 = age > R, pass 1 = age <= R.
-template <int K, bool VEC, bool MON>
-__device__ __forceinline__ void window_pass(const EpochArgs& a, uint32_t u, uint32_t j,
-                                            uint32_t c0, uint32_t c1, int pass, int lane,
-                                            uint32_t* qbuf, const double (&uu)[K],
-                                            double (&acc)[K], double& lsum) {
-  const uint64_t r0 = a.rowptr[u];
-  const uint32_t cb = a.cbase[u];
-  RowQueue<K, VEC, MON, true> q{qbuf, 0};
-  for (uint32_t c = c0; c < c1; ++c) {
-    const uint32_t m = __ldcg(a.wcnt + cb + c);
-    const uint64_t base = r0 + uint64_t(c) * a.C;
-    for (uint32_t k0 = 0; k0 < m; k0 += 32) {
-      const int cnt = int(umin32(32, m - k0));
-      bool use = false;
-      uint32_t pk = 0;
-      if (lane < cnt) {
-        const uint32_t v = __ldcg(a.wl + base + k0 + lane);
-        const uint32_t st = ld_relaxed(a.state + v);
-        const uint32_t age = j - (st >> 1);
-        use = pass == 0 ? age > a.R : age <= a.R;
-        if (use) {
-          wait_written(a.state, v, st);
-          pk = v | kNewBit;
-        }
-      }
-      q.push(a, lane, use, pk, uu, acc, lsum);
-    }
-  }
-  q.flush(a, lane, uu, acc, lsum);
-}
-
-template <int K, bool VEC, bool MON>
-__device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint32_t* qbuf) {
-  using L = Lay<K, VEC>;
-  const uint32_t u = a.perm[p];
-  const uint32_t j = p / a.b;
-  const uint32_t cb = a.cbase[u];
-  const uint32_t nch = a.cbase[u + 1] - cb;
-  const uint32_t nchL = a.lbase[u + 1] - a.lbase[u];
-  float zu[K];
-  L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
-  double uu[K], acc[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) { uu[k] = zu[k]; acc[k] = 0.0; }
-  double lsum = 0.0;
-  // the E work of u must be complete (its partial and window lists)
-  uint32_t f = ld_relaxed(a.vflag + u);
-  while (f == 0) {
-    __nanosleep(64);
-    f = ld_relaxed(a.vflag + u);
-  }
-  const uint32_t c0 = cl * a.G, c1 = umin32(nch, c0 + a.G);
-  if (nchL == 1) {  // E total + old window arcs + negatives + recent arcs
-    L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
-    if (MON) lsum = __ldcg(a.eloss + cb);
-    window_pass<K, VEC, MON>(a, u, j, c0, c1, 0, lane, qbuf, uu, acc, lsum);
-    do_negatives<K, VEC, MON>(a, j, lane, uu, acc, lsum);
-    window_pass<K, VEC, MON>(a, u, j, c0, c1, 1, lane, qbuf, uu, acc, lsum);
-    finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
-    if (lane == 0) a.vflag[u] = 0;
-    return;
-  }
-  window_pass<K, VEC, MON>(a, u, j, c0, c1, 0, lane, qbuf, uu, acc, lsum);
-  window_pass<K, VEC, MON>(a, u, j, c0, c1, 1, lane, qbuf, uu, acc, lsum);
-  const uint32_t slot = a.lpo[u] + cl;
-  L::store_acc(a.lpart + size_t(slot) * a.d, lane, a.d, acc);
-  if (MON && lane == 0) __stcg(a.lloss + slot, lsum);
-  __threadfence();
-  __syncwarp();
-  uint32_t last = 0;
-  if (lane == 0) last = atomicAdd(a.lcnt + u, 1u) == nchL - 1 ? 1u : 0u;
-  if (!__shfl_sync(kFull, last, 0)) return;
-  __threadfence();
-  L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
-  lsum = MON ? __ldcg(a.eloss + cb) : 0.0;
-  const uint32_t lp = a.lpo[u];
-#pragma unroll 4
-  for (uint32_t qq = 0; qq < nchL; ++qq) {
-    L::add_acc(a.lpart + size_t(lp + qq) * a.d, lane, a.d, acc);
-    if (MON) lsum = __dadd_rn(lsum, __ldcg(a.lloss + lp + qq));
-  }
-  do_negatives<K, VEC, MON>(a, j, lane, uu, acc, lsum);
-  finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
-  if (lane == 0) {
-    a.lcnt[u] = 0;
-    a.vflag[u] = 0;
-  }
-}
-
-template <int K, bool VEC, bool MON>
-__global__ void __launch_bounds__(kWarps * 32) epoch_kernel(EpochArgs a) {
-  __shared__ uint32_t qs[kWarps][kQ];
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  uint32_t* qbuf = qs[w];
-  const bool lrole = w >= kWarps - int(a.lwarps);
-  uint32_t* counter = a.next + (lrole ? 1 : 0);
-  const uint32_t total = lrole ? *a.n_litems : a.n_eitems;
-  const uint2* items = lrole ? a.litems : a.eitems;
-  uint32_t it = 0;
-  if (lane == 0) it = atomicAdd(counter, 1u);
-  it = __shfl_sync(kFull, it, 0);
-  while (it < total) {
-    uint32_t nxt = 0;
-    if (lane == 0) nxt = atomicAdd(counter, 1u);  // claim ahead: hides the atomic's latency
-    const uint2 item = items[it];
-    if (lrole) do_L<K, VEC, MON>(a, item.x, item.y, lane, qbuf);
-    else do_E<K, VEC, MON>(a, item.x, item.y, lane, qbuf);
-    it = __shfl_sync(kFull, nxt, 0);
-  }
-}
 
 // ------------------------------------------------------ per-epoch prep
 __global__ void state_kernel(const uint32_t* __restrict__ perm, uint32_t* __restrict__ state,
@@ -486,36 +136,6 @@ __global__ void restore_kernel(const uint32_t* __restrict__ state, const float* 
   if ((state[v] >> 1) >= jb) znew[t] = zold[t];
 }
 
-template <int K, bool VEC, bool MON>
-void launch_epoch_t(Ctx& c, const EpochArgs& a) {
-  auto kern = epoch_kernel<K, VEC, MON>;
-  int per_sm = 0;
-  F2V_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0));
-  if (per_sm < 1) per_sm = 1;
-  uint32_t blocks = uint32_t(per_sm) * uint32_t(c.num_sms);
-  const uint64_t ew = kWarps - a.lwarps;
-  const uint32_t need = uint32_t(std::max<uint64_t>((a.n_eitems + ew - 1) / ew, 1));
-  blocks = std::max(1u, std::min(blocks, need));
-  kern<<<blocks, kWarps * 32, 0, c.stream>>>(a);
-  F2V_CUDA(cudaGetLastError());
-  ++c.launches;
-}
-
-template <bool MON>
-void launch_epoch(Ctx& c, const EpochArgs& a) {
-  const uint32_t d = a.d;
-  if (d == 128) launch_epoch_t<4, true, MON>(c, a);
-  else if (d == 256) launch_epoch_t<8, true, MON>(c, a);
-  else if (d == 64) launch_epoch_t<2, true, MON>(c, a);
-  else if (d == 32) launch_epoch_t<1, true, MON>(c, a);
-  else if (d <= 32) launch_epoch_t<1, false, MON>(c, a);
-  else if (d <= 64) launch_epoch_t<2, false, MON>(c, a);
-  else if (d <= 128) launch_epoch_t<4, false, MON>(c, a);
-  else if (d <= 256) launch_epoch_t<8, false, MON>(c, a);
-  else if (d <= 512) launch_epoch_t<16, false, MON>(c, a);
-  else launch_epoch_t<32, false, MON>(c, a);
-}
-
 uint32_t env_u32(const char* name, uint32_t dflt) {
   if (const char* e = std::getenv(name)) {
     const long v = std::atol(e);
@@ -531,7 +151,8 @@ void load_tuning(EpochTuning& t) {
   t.lgroup = std::max(1u, env_u32("F2V_LGROUP", t.lgroup));
   t.window = std::max(1u, env_u32("F2V_WINDOW", t.window));
   t.recent = env_u32("F2V_RECENT", t.recent);
-  t.lwarps = std::min(uint32_t(kWarps - 1), std::max(1u, env_u32("F2V_LWARPS", t.lwarps)));
+  t.lwarps = std::min(uint32_t(ep::kWarps - 1), std::max(1u, env_u32("F2V_LWARPS", t.lwarps)));
+  if (const char* e = std::getenv("F2V_PRECISION")) t.fast = std::strcmp(e, "exact") != 0;
 }
 
 // Static per-graph chunk / L-group layout (depends on chunk and lgroup only).
@@ -661,7 +282,7 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   uint32_t* ctr = c.counters.as<uint32_t>();  // [0..1] claims, [2..3] bad, [4..5] loss, [8] nL
   F2V_CUDA(cudaMemsetAsync(ctr, 0, 8, c.stream));
   F2V_CUDA(cudaMemsetAsync(ctr + 2, 0xff, 8, c.stream));
-  EpochArgs a;
+  ep::EpochArgs a;
   a.rowptr = c.rowptr.as<uint64_t>();
   a.col = c.col.as<uint32_t>();
   a.zold = c.z[c.cur].as<float>();
@@ -713,8 +334,7 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
     F2V_CUDA(cudaEventCreate(&c.ev_kernel[1]));
   }
   F2V_CUDA(cudaEventRecord(c.ev_kernel[0], c.stream));
-  if (monitor) launch_epoch<true>(c, a);
-  else launch_epoch<false>(c, a);
+  ep::launch_epoch(c, a, monitor, c.tune.fast != 0);
   F2V_CUDA(cudaEventRecord(c.ev_kernel[1], c.stream));
   if (monitor) {
     sum_kernel<<<1, 1024, 0, c.stream>>>(c.ploss.as<double>(), c.n,

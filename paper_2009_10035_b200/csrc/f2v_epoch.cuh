@@ -1,0 +1,433 @@
+// f2v_epoch.cuh -- the persistent dataflow epoch kernel (see f2v_epoch.cu for
+// the schedule).  Instantiated per (force kind, row layout, loss monitoring,
+// precision) in f2v_epoch_fast.cu / f2v_epoch_exact.cu.
+#pragma once
+#include <algorithm>
+
+#include "f2v_internal.h"
+#include "f2v_pair.cuh"
+#include "f2v_rng.h"
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "f2v_internal.h"
+#include "f2v_pair.cuh"
+#include "f2v_rng.h"
+
+namespace f2v {
+namespace ep {
+
+using namespace dev;
+
+constexpr int kWarps = 8;       // warps per CTA
+constexpr int kQ = 64;          // per-warp compaction queue (entries)
+
+struct EpochArgs {
+  const uint64_t* rowptr;
+  const uint32_t* col;
+  const float* zold;
+  float* znew;
+  const uint32_t* perm;
+  uint32_t* state;
+  const uint32_t* negs;
+  const uint32_t* negwin;
+  const uint2* eitems;
+  const uint2* litems;
+  uint32_t n_eitems;
+  const uint32_t* n_litems;  // device count (written by the prep)
+  uint32_t* next;  // [0] E claims, [1] L claims
+  const uint32_t* cbase;
+  const uint32_t* lbase;
+  const uint32_t* lpo;
+  const uint32_t* needs;  // per vertex: window arcs/negatives exist
+  double* epart;
+  double* eloss;
+  uint32_t* wcnt;
+  uint32_t* wl;
+  double* lpart;
+  double* lloss;
+  uint32_t* ecnt;
+  uint32_t* lcnt;
+  uint32_t* vflag;
+  double* ploss;
+  unsigned long long* bad;
+  uint32_t n, d, b, s;
+  uint32_t C, G, W, R, lwarps;
+  float eta;
+  ForceParams fp;
+  int nodep;                    // DEBUG (F2V_DEBUG_NODEP): every row read from Zold, no waits
+  unsigned long long* trace;    // DEBUG (F2V_TRACE): per position finalise time (ns)
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t wait_written(const uint32_t* state, uint32_t v, uint32_t st) {
+  while (!(st & 1u)) {
+    __nanosleep(32);
+    st = ld_relaxed(state + v);
+  }
+  return st;
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
+
+// Per-warp FIFO of packed row ids (bit 31 = Znew) in shared memory; rows
+// are accumulated 32 at a time in push order (= the deterministic pair order).
+template <int KIND, int K, bool VEC, bool MON, bool FAST, bool ATT>
+struct RowQueue {
+  uint32_t* buf;
+  int n;
+  __device__ __forceinline__ void push(const EpochArgs& a, int lane, bool keep, uint32_t val,
+                                       const float (&zu)[K], double (&acc)[K], double& lsum) {
+    const uint32_t m = __ballot_sync(kFull, keep);
+    if (keep) buf[n + __popc(m & lanemask_lt(lane))] = val;
+    __syncwarp();
+    n += __popc(m);
+    if (n >= 32) {
+      const uint32_t pk = buf[lane];
+      const uint32_t rest = lane + 32 < n ? buf[lane + 32] : 0u;
+      __syncwarp();
+      buf[lane] = rest;
+      __syncwarp();
+      n -= 32;
+      Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, 32, lane, a.d, a.zold, a.znew,
+                                                       zu, acc, lsum);
+    }
+  }
+  __device__ __forceinline__ void flush(const EpochArgs& a, int lane, const float (&zu)[K],
+                                        double (&acc)[K], double& lsum) {
+    if (n == 0) return;
+    const uint32_t pk = lane < n ? buf[lane] : 0u;
+    __syncwarp();
+    const int cnt = n;
+    n = 0;
+    Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew, zu,
+                                                     acc, lsum);
+  }
+};
+
+// The shared negatives of batch j, in sample order (sampling.cpp:59).
+template <int KIND, int K, bool VEC, bool MON, bool FAST>
+__device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, int lane,
+                                             const float (&zu)[K], double (&acc)[K],
+                                             double& lsum) {
+  for (uint32_t k0 = 0; k0 < a.s; k0 += 32) {
+    const int cnt = int(umin32(32, a.s - k0));
+    uint32_t pk = 0;
+    if (lane < cnt) {
+      const uint32_t w = a.negs[size_t(j) * a.s + k0 + lane];
+      const uint32_t st = ld_relaxed(a.state + w);
+      if ((st >> 1) < j && !a.nodep) {
+        wait_written(a.state, w, st);
+        pk = w | kNewBit;
+      } else {
+        pk = w;
+      }
+    }
+    Rows<KIND, K, VEC, MON, FAST>::template run<false>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew,
+                                                       zu, acc, lsum);
+  }
+}
+
+// g = float(acc) (trainer.cpp:140-145); z_u -= eta*g in fp32 (trainer.cpp:173);
+// publish row u of Znew.
+template <int K, bool VEC, bool MON>
+__device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_t u, int lane,
+                                         const float (&zu)[K], const double (&acc)[K],
+                                         double lsum) {
+  using L = Lay<K, VEC>;
+  bool bad = false;
+  float nz[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const float g = __double2float_rn(acc[k]);
+    if (L::valid(lane, k, a.d) && !isfinite(g)) bad = true;
+    nz[k] = __fsub_rn(zu[k], __fmul_rn(a.eta, g));
+  }
+  L::store(a.znew + size_t(u) * a.d, lane, a.d, nz);
+  const bool any_bad = __any_sync(kFull, bad);
+  if (MON) {
+    const double tot = warp_sum_d(lsum);
+    if (lane == 0) a.ploss[p] = tot;
+  }
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) {
+    if (any_bad) atomicMin(a.bad, (unsigned long long)p);
+    atomicOr(a.state + u, 1u);
+    if (a.trace) a.trace[p] = globaltimer();
+  }
+}
+
+template <int KIND, int K, bool VEC, bool MON, bool FAST>
+__device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint32_t* qbuf) {
+  using L = Lay<K, VEC>;
+  const uint32_t u = a.perm[p];
+  const uint32_t j = p / a.b;
+  const uint64_t r0 = a.rowptr[u], r1 = a.rowptr[u + 1];
+  const uint32_t cb = a.cbase[u];
+  const uint32_t nch = a.cbase[u + 1] - cb;
+  const uint32_t cs = cb + c;
+  const uint64_t e0 = r0 + uint64_t(c) * a.C;
+  const uint64_t e1 = umin64(e0 + a.C, r1);
+  float zu[K];
+  L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  double lsum = 0.0;
+  uint32_t wc = 0;
+  RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0};
+  for (uint64_t e = e0; e < e1; e += 32) {
+    const int cnt = int(umin64(32, e1 - e));
+    uint32_t v = 0, pk = 0;
+    bool use = false, win = false;
+    if (lane < cnt) {
+      v = a.col[e + lane];
+      const uint32_t st = ld_relaxed(a.state + v);
+      const uint32_t bv = st >> 1;
+      if (bv >= j || a.nodep) {
+        use = true;
+        pk = v;
+      } else if (bv + a.W < j) {  // past: final long ago (rarely waits)
+        wait_written(a.state, v, st);
+        use = true;
+        pk = v | kNewBit;
+      } else {
+        win = true;
+      }
+    }
+    const uint32_t wm = __ballot_sync(kFull, win);
+    if (win) a.wl[e0 + wc + __popc(wm & lanemask_lt(lane))] = v;
+    wc += __popc(wm);
+    q.push(a, lane, use, pk, zu, acc, lsum);
+  }
+  q.flush(a, lane, zu, acc, lsum);
+  const bool needs = a.needs[u] != 0;
+  if (nch == 1) {
+    if (!needs) {
+      do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+      finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
+    } else {
+      L::store_acc(a.epart + size_t(cs) * a.d, lane, a.d, acc);
+      const double ls = MON ? warp_sum_d(lsum) : 0.0;
+      if (lane == 0) {
+        if (MON) __stcg(a.eloss + cs, ls);
+        __stcg(a.wcnt + cs, wc);
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_relaxed(a.vflag + u, 1u);
+    }
+    return;
+  }
+  // hub chunk: publish the partial; the last E arrival combines in chunk order
+  L::store_acc(a.epart + size_t(cs) * a.d, lane, a.d, acc);
+  {
+    const double ls = MON ? warp_sum_d(lsum) : 0.0;
+    if (lane == 0) {
+      if (MON) __stcg(a.eloss + cs, ls);
+      __stcg(a.wcnt + cs, wc);
+    }
+  }
+  __threadfence();
+  __syncwarp();
+  uint32_t last = 0;
+  if (lane == 0) last = atomicAdd(a.ecnt + u, 1u) == nch - 1 ? 1u : 0u;
+  if (!__shfl_sync(kFull, last, 0)) return;
+  __threadfence();
+  L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
+  lsum = (MON && lane == 0) ? __ldcg(a.eloss + cb) : 0.0;
+#pragma unroll 4
+  for (uint32_t qq = 1; qq < nch; ++qq) {
+    L::add_acc(a.epart + size_t(cb + qq) * a.d, lane, a.d, acc);
+    if (MON && lane == 0) lsum = __dadd_rn(lsum, __ldcg(a.eloss + cb + qq));
+  }
+  if (lane == 0) a.ecnt[u] = 0;
+  if (!needs) {
+    do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+    finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
+  } else {
+    L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);  // the E total
+    if (MON && lane == 0) __stcg(a.eloss + cb, lsum);  // lane 0 holds the whole sum here
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_relaxed(a.vflag + u, 1u);
+  }
+}
+
+// Window arcs of chunks [c0, c1) of u: pass 0 = age > R, pass 1 = age <= R.
+template <int KIND, int K, bool VEC, bool MON, bool FAST>
+__device__ __forceinline__ void window_pass(const EpochArgs& a, uint32_t u, uint32_t j,
+                                            uint32_t c0, uint32_t c1, int pass, int lane,
+                                            uint32_t* qbuf, const float (&zu)[K],
+                                            double (&acc)[K], double& lsum) {
+  const uint64_t r0 = a.rowptr[u];
+  const uint32_t cb = a.cbase[u];
+  RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0};
+  for (uint32_t c = c0; c < c1; ++c) {
+    const uint32_t m = __ldcg(a.wcnt + cb + c);
+    const uint64_t base = r0 + uint64_t(c) * a.C;
+    for (uint32_t k0 = 0; k0 < m; k0 += 32) {
+      const int cnt = int(umin32(32, m - k0));
+      bool use = false;
+      uint32_t pk = 0;
+      if (lane < cnt) {
+        const uint32_t v = __ldcg(a.wl + base + k0 + lane);
+        const uint32_t st = ld_relaxed(a.state + v);
+        const uint32_t age = j - (st >> 1);
+        use = pass == 0 ? age > a.R : age <= a.R;
+        if (use) {
+          wait_written(a.state, v, st);
+          pk = v | kNewBit;
+        }
+      }
+      q.push(a, lane, use, pk, zu, acc, lsum);
+    }
+  }
+  q.flush(a, lane, zu, acc, lsum);
+}
+
+template <int KIND, int K, bool VEC, bool MON, bool FAST>
+__device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint32_t* qbuf) {
+  using L = Lay<K, VEC>;
+  const uint32_t u = a.perm[p];
+  const uint32_t j = p / a.b;
+  const uint32_t cb = a.cbase[u];
+  const uint32_t nch = a.cbase[u + 1] - cb;
+  const uint32_t nchL = a.lbase[u + 1] - a.lbase[u];
+  float zu[K];
+  L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
+  double acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  double lsum = 0.0;
+  // the E work of u must be complete (its partial and window lists)
+  uint32_t f = ld_relaxed(a.vflag + u);
+  while (f == 0) {
+    __nanosleep(64);
+    f = ld_relaxed(a.vflag + u);
+  }
+  const uint32_t c0 = cl * a.G, c1 = umin32(nch, c0 + a.G);
+  if (nchL == 1) {  // E total + old window arcs + negatives + recent arcs
+    L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
+    if (MON && lane == 0) lsum = __ldcg(a.eloss + cb);
+    window_pass<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, 0, lane, qbuf, zu, acc, lsum);
+    do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+    window_pass<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, 1, lane, qbuf, zu, acc, lsum);
+    finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
+    if (lane == 0) a.vflag[u] = 0;
+    return;
+  }
+  window_pass<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, 0, lane, qbuf, zu, acc, lsum);
+  window_pass<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, 1, lane, qbuf, zu, acc, lsum);
+  const uint32_t slot = a.lpo[u] + cl;
+  L::store_acc(a.lpart + size_t(slot) * a.d, lane, a.d, acc);
+  {
+    const double ls = MON ? warp_sum_d(lsum) : 0.0;
+    if (MON && lane == 0) __stcg(a.lloss + slot, ls);
+  }
+  __threadfence();
+  __syncwarp();
+  uint32_t last = 0;
+  if (lane == 0) last = atomicAdd(a.lcnt + u, 1u) == nchL - 1 ? 1u : 0u;
+  if (!__shfl_sync(kFull, last, 0)) return;
+  __threadfence();
+  L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
+  lsum = (MON && lane == 0) ? __ldcg(a.eloss + cb) : 0.0;
+  const uint32_t lp = a.lpo[u];
+#pragma unroll 4
+  for (uint32_t qq = 0; qq < nchL; ++qq) {
+    L::add_acc(a.lpart + size_t(lp + qq) * a.d, lane, a.d, acc);
+    if (MON && lane == 0) lsum = __dadd_rn(lsum, __ldcg(a.lloss + lp + qq));
+  }
+  do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+  finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
+  if (lane == 0) {
+    a.lcnt[u] = 0;
+    a.vflag[u] = 0;
+  }
+}
+
+template <int KIND, int K, bool VEC, bool MON, bool FAST>
+__global__ void __launch_bounds__(kWarps * 32, 2) epoch_kernel(EpochArgs a) {
+  __shared__ uint32_t qs[kWarps][kQ];
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  uint32_t* qbuf = qs[w];
+  const bool lrole = w >= kWarps - int(a.lwarps);
+  uint32_t* counter = a.next + (lrole ? 1 : 0);
+  const uint32_t total = lrole ? *a.n_litems : a.n_eitems;
+  const uint2* items = lrole ? a.litems : a.eitems;
+  uint32_t it = 0;
+  if (lane == 0) it = atomicAdd(counter, 1u);
+  it = __shfl_sync(kFull, it, 0);
+  while (it < total) {
+    uint32_t nxt = 0;
+    if (lane == 0) nxt = atomicAdd(counter, 1u);  // claim ahead: hides the atomic's latency
+    const uint2 item = items[it];
+    if (lrole) do_L<KIND, K, VEC, MON, FAST>(a, item.x, item.y, lane, qbuf);
+    else do_E<KIND, K, VEC, MON, FAST>(a, item.x, item.y, lane, qbuf);
+    it = __shfl_sync(kFull, nxt, 0);
+  }
+}
+
+// Launch one epoch kernel instantiation as a persistent grid.
+template <int KIND, int K, bool VEC, bool MON, bool FAST>
+void launch_one(Ctx& c, const EpochArgs& a) {
+  auto kern = epoch_kernel<KIND, K, VEC, MON, FAST>;
+  int per_sm = 0;
+  F2V_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0));
+  if (per_sm < 1) per_sm = 1;
+  uint32_t blocks = uint32_t(per_sm) * uint32_t(c.num_sms);
+  const uint64_t ew = kWarps - a.lwarps;
+  const uint32_t need = uint32_t(std::max<uint64_t>((a.n_eitems + ew - 1) / ew, 1));
+  blocks = std::max(1u, std::min(blocks, need));
+  kern<<<blocks, kWarps * 32, 0, c.stream>>>(a);
+  F2V_CUDA(cudaGetLastError());
+  ++c.launches;
+}
+
+template <int KIND, int K, bool VEC, bool FAST>
+void launch_mon(Ctx& c, const EpochArgs& a, bool mon) {
+  if (mon) launch_one<KIND, K, VEC, true, FAST>(c, a);
+  else launch_one<KIND, K, VEC, false, FAST>(c, a);
+}
+
+template <int K, bool VEC, bool FAST>
+void launch_kind(Ctx& c, const EpochArgs& a, bool mon) {
+  switch (a.fp.kind) {
+    case F2V_SIGMOID: launch_mon<F2V_SIGMOID, K, VEC, FAST>(c, a, mon); break;
+    case F2V_TDIST: launch_mon<F2V_TDIST, K, VEC, FAST>(c, a, mon); break;
+    case F2V_FR: launch_mon<F2V_FR, K, VEC, FAST>(c, a, mon); break;
+    case F2V_FA: launch_mon<F2V_FA, K, VEC, FAST>(c, a, mon); break;
+    default: launch_mon<F2V_LINLOG, K, VEC, FAST>(c, a, mon); break;
+  }
+}
+
+// instantiation translation units (f2v_epoch_i_*.cu, compiled in parallel)
+void launch_fast_k4(Ctx& c, const EpochArgs& a, bool mon);
+void launch_fast_k2(Ctx& c, const EpochArgs& a, bool mon);
+void launch_fast_k8(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_vec(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_any(Ctx& c, const EpochArgs& a, bool mon);
+
+// d = 64/128/256 run FAST when asked; everything else runs EXACT.
+inline void launch_epoch(Ctx& c, const EpochArgs& a, bool mon, bool fast) {
+  if (fast && a.d == 128) launch_fast_k4(c, a, mon);
+  else if (fast && a.d == 64) launch_fast_k2(c, a, mon);
+  else if (fast && a.d == 256) launch_fast_k8(c, a, mon);
+  else if (a.d == 32 || a.d == 64 || a.d == 128 || a.d == 256) launch_exact_vec(c, a, mon);
+  else launch_exact_any(c, a, mon);
+}
+
+}  // namespace ep
+}  // namespace f2v
+

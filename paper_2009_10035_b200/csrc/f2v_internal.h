@@ -45,6 +45,7 @@ struct EpochTuning {
   uint32_t window = 48;  // F2V_WINDOW: arcs to batches [j-window, j) go to L items
   uint32_t recent = 2;   // F2V_RECENT: window arcs this recent are taken last
   uint32_t lwarps = 2;   // F2V_LWARPS: L-role warps per 8-warp CTA
+  uint32_t fast = 1;     // F2V_PRECISION=exact|fast: pair math precision (config)
 };
 void load_tuning(EpochTuning& t);
 

@@ -124,11 +124,11 @@ struct Term {
 // red = <u,o> (sigmoid) or ||u-o||^2 (distance kinds); nw2 = ||o||^2 for the
 // clamped sigmoid repulsion (force_kernels.cpp:95).
 template <bool MON>
-__device__ __forceinline__ Term pair_term(const ForceParams& fp, bool attractive, double red,
-                                          double nw2) {
+__device__ __forceinline__ Term pair_term(int kind, const ForceParams& fp, bool attractive,
+                                          double red, double nw2) {
   Term t{};
   t.scale = 1.0;
-  if (fp.kind == F2V_SIGMOID) {  // force_kernels.cpp:79-97
+  if (kind == F2V_SIGMOID) {  // force_kernels.cpp:79-97
     const double x = red;
     const double sg = stable_sigmoid(x);
     t.coef = attractive ? __dsub_rn(sg, 1.0) : sg;
@@ -149,7 +149,7 @@ __device__ __forceinline__ Term pair_term(const ForceParams& fp, bool attractive
   const double r_raw = sqrt(red);  // distance(), force_kernels.cpp:36-43
   double scalar;
   bool clamp_it = false;
-  if (fp.kind == F2V_TDIST) {
+  if (kind == F2V_TDIST) {
     if (attractive) {  // 99-107
       scalar = __ddiv_rn(__dmul_rn(2.0, r_raw), __dadd_rn(1.0, __dmul_rn(r_raw, r_raw)));
     } else {  // 109-119
@@ -168,8 +168,8 @@ __device__ __forceinline__ Term pair_term(const ForceParams& fp, bool attractive
     }
   } else {  // table-II kinds, force_kernels.cpp:121-147
     if (attractive) {
-      scalar = fp.kind == F2V_FR ? __dmul_rn(r_raw, r_raw)
-                                 : (fp.kind == F2V_FA ? r_raw : log1p(r_raw));
+      scalar = kind == F2V_FR ? __dmul_rn(r_raw, r_raw)
+                              : (kind == F2V_FA ? r_raw : log1p(r_raw));
     } else {
       scalar = __ddiv_rn(-1.0, dmax(r_raw, fp.eps));
       clamp_it = true;
@@ -223,16 +223,20 @@ __device__ __forceinline__ void accumulate(const Term& t, int lane, const double
 
 // Accumulate the pairs of `cnt` (<= 32) other-rows whose packed ids sit one per
 // lane (bit 31 = read the coherent Znew buffer), in lane order, U at a time.
-// Each row is converted to fp64 once and reused by the reduction and the axpy.
-template <int K, bool VEC, int U, bool MON, bool ATT>
-__device__ __forceinline__ void accumulate_rows(const ForceParams& fp, uint32_t packed, int cnt,
-                                                int lane, uint32_t d,
-                                                const float* __restrict__ zold,
-                                                const float* __restrict__ znew,
-                                                const double (&uu)[K], double (&acc)[K],
-                                                double& lsum) {
+// EXACT: everything fp64 in the reference's operation order (bitwise parity
+// in practice).  KIND < 0 = force kind chosen at run time.
+// lsum is a per-lane loss partial: the caller warp-sums it.
+template <int KIND, int K, bool VEC, int U, bool MON, bool ATT>
+__device__ __forceinline__ void rows_exact(const ForceParams& fp, uint32_t packed, int cnt,
+                                           int lane, uint32_t d, const float* __restrict__ zold,
+                                           const float* __restrict__ znew, const float (&zu)[K],
+                                           double (&acc)[K], double& lsum) {
   using L = Lay<K, VEC>;
-  const bool sig = fp.kind == F2V_SIGMOID;
+  const int kind = KIND >= 0 ? KIND : fp.kind;
+  const bool sig = kind == F2V_SIGMOID;
+  double uu[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) uu[k] = zu[k];
   for (int k0 = 0; k0 < cnt; k0 += U) {
     float v[U][K];
 #pragma unroll
@@ -276,12 +280,194 @@ __device__ __forceinline__ void accumulate_rows(const ForceParams& fp, uint32_t 
 #pragma unroll
     for (int i = 0; i < U; ++i) {
       if (k0 + i < cnt) {
-        const Term t = pair_term<MON>(fp, ATT, red[i], nw[i]);
+        const Term t = pair_term<MON>(kind, fp, ATT, red[i], nw[i]);
         accumulate<K>(t, lane, w[i], acc);
-        if (MON) lsum = __dadd_rn(lsum, t.loss);
+        if (MON && lane == 0) lsum = __dadd_rn(lsum, t.loss);
       }
     }
   }
+}
+
+// ------------------------------------------------------------ FAST mode
+// fp32 per-pair math (dot / distance, coefficient, axpy) with fp64
+// accumulation: every block of 8 pairs is summed in fp32 registers and then
+// added into the fp64 accumulator, so rounding error does not grow with the
+// degree (fp32 dot + fp64 accumulate stays within
+// ~3e-7 row-relative of the reference).  The 8 partial reductions of a block
+// are reduced "transposed": 4+2+1 exchange rounds leave each 4-lane group with
+// one pair's total, so the scalar force term of 8 pairs is evaluated once, in
+// parallel, and broadcast back.
+struct FastTerm {
+  float q;     // out_j = q * w_j   (w = o for sigmoid, u - o otherwise)
+  float fb;    // coincident fallback: out = (fb, 0, ..., 0), q = 0
+  float loss;
+};
+
+template <int KIND, bool ATT, bool MON>
+__device__ __forceinline__ FastTerm fast_term(const ForceParams& fp, float red, float nw2) {
+  FastTerm t{0.f, 0.f, 0.f};
+  const float eps = float(fp.eps), cap = float(fp.cap);
+  if (KIND == F2V_SIGMOID) {  // force_kernels.cpp:79-97, 213-219
+    const float x = red;
+    const float e = __expf(-fabsf(x));
+    const float inv = __fdividef(1.0f, 1.0f + e);
+    if (ATT) {
+      t.q = x >= 0.f ? -e * inv : -inv;  // sigma(x) - 1
+      if (MON) t.loss = x >= 0.f ? log1pf(e) : -x + log1pf(e);
+    } else {
+      const float sg = x >= 0.f ? inv : e * inv;
+      t.q = sg;
+      if (fp.has_cap) {
+        const float m = sg * sqrtf(nw2);
+        if (!(m <= cap || m == 0.f)) t.q = sg * __fdividef(cap, m);
+      }
+      if (MON) t.loss = x >= 0.f ? x + log1pf(e) : log1pf(e);
+    }
+    return t;
+  }
+  const float s = red;
+  if (KIND == F2V_TDIST && ATT) {  // force_kernels.cpp:99-107: (2t/(1+t^2)) (u-v)/t
+    if (s < eps * eps) t.fb = 2.0f * sqrtf(s) / (1.0f + s);
+    else t.q = __fdividef(2.0f, 1.0f + s);
+    if (MON) t.loss = log1pf(s);
+    return t;
+  }
+  const float r = sqrtf(s);
+  float scalar;
+  if (KIND == F2V_TDIST) {  // repulsive, force_kernels.cpp:109-119
+    const float tt = fmaxf(r, eps);
+    scalar = __fdividef(-2.0f, tt * (1.0f + tt * tt));
+    if (MON) {
+      const float tc = fmaxf(s, eps * eps);
+      t.loss = -logf(__fdividef(tc, 1.0f + tc));
+    }
+  } else if (ATT) {  // table-II attraction, force_kernels.cpp:121-134
+    scalar = KIND == F2V_FR ? s : (KIND == F2V_FA ? r : log1pf(r));
+  } else {
+    scalar = __fdividef(-1.0f, fmaxf(r, eps));
+  }
+  if (!ATT && fp.has_cap) {
+    const float m = fabsf(scalar);
+    if (!(m <= cap || m == 0.f)) scalar *= __fdividef(cap, m);
+  }
+  if (r < eps) t.fb = scalar;
+  else t.q = __fdividef(scalar, r);
+  return t;
+}
+
+// Transposed reduction of 8 per-lane partials: returns, on every lane, the
+// warp total of partial number pair_of_lane(lane).
+__device__ __forceinline__ float reduce8(float (&p)[8], int lane) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool hi = lane & 16;
+    const float send = hi ? p[i] : p[i + 4];
+    const float keep = hi ? p[i + 4] : p[i];
+    p[i] = keep + __shfl_xor_sync(kFull, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool hi = lane & 8;
+    const float send = hi ? p[i] : p[i + 2];
+    const float keep = hi ? p[i + 2] : p[i];
+    p[i] = keep + __shfl_xor_sync(kFull, send, 8);
+  }
+  {
+    const bool hi = lane & 4;
+    const float send = hi ? p[0] : p[1];
+    const float keep = hi ? p[1] : p[0];
+    p[0] = keep + __shfl_xor_sync(kFull, send, 4);
+  }
+  p[0] += __shfl_xor_sync(kFull, p[0], 2);
+  p[0] += __shfl_xor_sync(kFull, p[0], 1);
+  return p[0];
+}
+__device__ __forceinline__ int pair_of_lane(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+}
+__device__ __forceinline__ int lane_of_pair(int i) {
+  return (((i >> 2) & 1) << 4) | (((i >> 1) & 1) << 3) | ((i & 1) << 2);
+}
+
+template <int KIND, int K, bool MON, bool ATT>
+__device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed, int cnt,
+                                          int lane, uint32_t d, const float* __restrict__ zold,
+                                          const float* __restrict__ znew, const float (&zu)[K],
+                                          double (&acc)[K], double& lsum) {
+  using L = Lay<K, true>;
+  constexpr bool SIG = KIND == F2V_SIGMOID;
+  const int pi = pair_of_lane(lane);
+  for (int k0 = 0; k0 < cnt; k0 += 8) {
+    float w[8][K];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
+      if (k0 + i < cnt) {
+        const bool coh = (pk & kNewBit) != 0;
+        L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, w[i], coh);
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) w[i][k] = 0.0f;
+      }
+    }
+    float part[8], nrm[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float s = 0.f, q = 0.f;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (SIG) {
+          s = fmaf(zu[k], w[i][k], s);
+          if (!ATT) q = fmaf(w[i][k], w[i][k], q);
+        } else {
+          w[i][k] = zu[k] - w[i][k];
+          s = fmaf(w[i][k], w[i][k], s);
+        }
+      }
+      part[i] = s;
+      nrm[i] = q;
+    }
+    const float red = reduce8(part, lane);
+    const float nr = (SIG && !ATT) ? reduce8(nrm, lane) : 0.f;
+    const FastTerm t = fast_term<KIND, ATT, MON>(fp, red, nr);
+    if (MON && (lane & 3) == 0 && k0 + pi < cnt) lsum = __dadd_rn(lsum, double(t.loss));
+    float a32[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) a32[k] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float qi = __shfl_sync(kFull, t.q, lane_of_pair(i));
+      const float fbi = SIG ? 0.f : __shfl_sync(kFull, t.fb, lane_of_pair(i));
+      if (k0 + i < cnt) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) a32[k] = fmaf(qi, w[i][k], a32[k]);
+        if (!SIG && lane == 0) a32[0] += fbi;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = __dadd_rn(acc[k], double(a32[k]));
+  }
+}
+
+// The row-accumulation policy the epoch kernel is instantiated with.
+template <int KIND, int K, bool VEC, bool MON, bool FAST>
+struct Rows {
+  template <bool ATT>
+  __device__ static __forceinline__ void run(const ForceParams& fp, uint32_t packed, int cnt,
+                                             int lane, uint32_t d, const float* zold,
+                                             const float* znew, const float (&zu)[K],
+                                             double (&acc)[K], double& lsum) {
+    if constexpr (FAST)
+      rows_fast<KIND, K, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
+    else
+      rows_exact<KIND, K, VEC, 4, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
+  }
+};
+
+__device__ __forceinline__ double warp_sum_d(double x) {
+#pragma unroll
+  for (int m = 16; m; m >>= 1) x = __dadd_rn(x, __shfl_xor_sync(kFull, x, m));
+  return x;
 }
 
 }  // namespace dev

@@ -37,20 +37,20 @@ __global__ void __launch_bounds__(256) grad_step_kernel(StepArgs a) {
   const uint32_t u = a.ids[i];
   float zu[K];
   L::load(a.z + size_t(u) * a.d, lane, a.d, zu, false);
-  double uu[K], acc[K];
+  double acc[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) { uu[k] = zu[k]; acc[k] = 0.0; }
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
   double lsum = 0.0;
   const uint64_t r0 = a.rowptr[u], r1 = a.rowptr[u + 1];
   for (uint64_t e = r0; e < r1; e += 32) {
     const int cnt = int(umin64(32, r1 - e));
     const uint32_t v = lane < cnt ? a.col[e + lane] : 0u;
-    accumulate_rows<K, VEC, 4, MON, true>(a.fp, v, cnt, lane, a.d, a.z, a.z, uu, acc, lsum);
+    rows_exact<-1, K, VEC, 4, MON, true>(a.fp, v, cnt, lane, a.d, a.z, a.z, zu, acc, lsum);
   }
   for (uint32_t k0 = 0; k0 < a.s; k0 += 32) {
     const int cnt = int(umin32(32, a.s - k0));
     const uint32_t w = lane < cnt ? a.negs[k0 + lane] : 0u;
-    accumulate_rows<K, VEC, 4, MON, false>(a.fp, w, cnt, lane, a.d, a.z, a.z, uu, acc, lsum);
+    rows_exact<-1, K, VEC, 4, MON, false>(a.fp, w, cnt, lane, a.d, a.z, a.z, zu, acc, lsum);
   }
   float g[K];
   bool bad = false;
@@ -61,7 +61,10 @@ __global__ void __launch_bounds__(256) grad_step_kernel(StepArgs a) {
   }
   L::store(a.grads + size_t(i) * a.d, lane, a.d, g);
   if (__any_sync(kFull, bad) && lane == 0) atomicMin(a.bad, (unsigned long long)i);
-  if (MON && lane == 0) a.vloss[i] = lsum;
+  if (MON) {
+    const double tot = warp_sum_d(lsum);
+    if (lane == 0) a.vloss[i] = tot;
+  }
 }
 
 // apply_update, distinct ids: one thread per element (fp32 mul then sub).
