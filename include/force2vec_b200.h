@@ -169,6 +169,10 @@ int32_t f2v_csr_from_edges(const uint32_t* pairs, uint64_t m, uint32_t n, int32_
 /* partition_epoch (sampling.cpp:7-19) for train()'s key (seed,{0x22,epoch}) */
 int32_t f2v_partition_epoch(uint32_t n, uint32_t b, uint64_t seed, uint32_t epoch,
                             uint32_t* perm_out);
+/* the same permutation computed on the device (deterministic-reservation
+ * Fisher-Yates, bit-identical); the one train_epochs uses every epoch */
+int32_t f2v_device_partition_epoch(f2v_ctx* ctx, uint32_t n, uint32_t b, uint64_t seed,
+                                   uint32_t epoch, uint32_t* perm_out);
 /* the negatives of (epoch, batch[, shard]) under a sampler, host side */
 int32_t f2v_negatives(int32_t sampler, uint64_t seed, uint32_t epoch, uint64_t batch,
                       uint32_t shard, uint32_t num_shards, uint32_t n, uint32_t s,

@@ -129,6 +129,8 @@ SYMBOLS = {
                                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                   C.POINTER(C.c_uint64)]),
     "f2v_partition_epoch": (_i32, [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, _u32p]),
+    "f2v_device_partition_epoch": (_i32, [_vp, C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32,
+                                          _u32p]),
     "f2v_negatives": (_i32, [_i32, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
                              C.c_uint32, C.c_uint32, _u32p]),
     "f2v_gen_sbm": (_i32, [C.c_uint32, _i32, C.c_double, C.c_double, C.c_uint64,
@@ -397,6 +399,12 @@ class Device:
         self._ck(_lib.f2v_last_timing(self._h, out))
         return {"device_ms": out[0], "epoch_kernel_ms": out[1], "epoch_kernels": int(out[2]),
                 "host_ms": out[3]}
+
+    def partition_epoch(self, n: int, b: int, seed: int, epoch: int) -> np.ndarray:
+        """partition_epoch (sampling.cpp:7-19) computed on the device."""
+        perm = np.zeros(n, np.uint32)
+        self._ck(_lib.f2v_device_partition_epoch(self._h, n, b, seed, epoch, perm))
+        return perm
 
     def upload_graph(self, g: CsrGraph):
         self._ck(_lib.f2v_upload_graph(self._h, g.num_vertices(), g.row_offsets,

@@ -34,6 +34,22 @@ def deps():
         os.path.join(os.path.dirname(PKG), "include", "force2vec_b200.h")]
 
 
+def _obj(src):
+    return os.path.join(LIBDIR, "obj", os.path.basename(src) + ".o")
+
+
+def _headers():
+    return [f for f in deps() if not f.endswith((".cu", ".cpp"))]
+
+
+def _stale(src):
+    obj = _obj(src)
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return os.path.getmtime(src) > t or any(os.path.getmtime(h) > t for h in _headers())
+
+
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
@@ -49,18 +65,23 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(tmpdir, exist_ok=True)
     jobs = []
     for src in sources():
-        obj = os.path.join(tmpdir, os.path.basename(src) + ".o")
+        obj = _obj(src)
+        if not force and not _stale(src):
+            continue
         cmd = ["nvcc", *NVCC_FLAGS, "-c", src, "-o", obj]
         if verbose and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
         jobs.append((cmd, obj))
-    # translation units compile in parallel (the epoch kernel has many
-    # instantiations split across files)
+    # translation units compile in parallel (the epoch kernel's instantiations
+    # are split across files); objects newer than their sources are reused
     procs = [(subprocess.Popen(cmd), obj) for cmd, obj in jobs]
     for p, obj in procs:
         if p.wait() != 0:
             raise subprocess.CalledProcessError(p.returncode, "nvcc " + obj)
-    objs = [obj for _, obj in procs]
+    objs = [_obj(src) for src in sources()]
+    for o in list(os.listdir(tmpdir)):  # drop objects of deleted sources
+        if os.path.join(tmpdir, o) not in objs:
+            os.remove(os.path.join(tmpdir, o))
     cmd = ["nvcc", *ARCH, "-shared", "-o", LIB + ".tmp", *objs, "-Xcompiler", "-pthread"]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)

@@ -7,7 +7,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
-#include <future>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -181,35 +181,20 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
   const ForceParams fp = make_params(cfg.model);
   const uint64_t nb = (uint64_t(n) + b - 1) / b;
   c.perm.ensure(sizeof(uint32_t) * n);
-  uint32_t* hperm = nullptr;
-  F2V_CUDA(cudaMallocHost(&hperm, sizeof(uint32_t) * n * 2));
-  struct Pinned {
-    uint32_t* p;
-    ~Pinned() { cudaFreeHost(p); }
-  } pin{hperm};
-  auto make_perm = [&](uint32_t e, uint32_t* out) {
-    partition_epoch(n, b, rng_keyed2(cfg.seed, kStreamPartition, e), out);
-  };
-  make_perm(cfg.first_epoch, hperm);
   uint64_t attr = 0, rep = 0;
   for (uint32_t e = cfg.first_epoch; e < end_epoch; ++e) {
-    uint32_t* cur_perm = hperm + size_t((e - cfg.first_epoch) & 1) * n;
-    uint32_t* nxt_perm = hperm + size_t((e - cfg.first_epoch + 1) & 1) * n;
     float eta = cfg.lr;
     if (cfg.lr_decay) eta = cfg.lr * (1.0f - float(e) / float(cfg.epochs));
-    F2V_CUDA(cudaMemcpyAsync(c.perm.p, cur_perm, sizeof(uint32_t) * n, cudaMemcpyHostToDevice,
-                             c.stream));
+    // partition_epoch (trainer.cpp:216-217) as a device Fisher-Yates
+    k_device_partition(c, n, cfg.seed, e, c.perm.as<uint32_t>());
     k_epoch_begin(c, b, s, e, cfg.seed, cfg.sampler);
-    // next epoch's Fisher-Yates overlaps this epoch's kernels
-    std::future<void> fut;
-    if (e + 1 < end_epoch)
-      fut = std::async(std::launch::async, [&, e] { make_perm(e + 1, nxt_perm); });
     const EpochResult r = k_epoch_run(c, b, s, eta, fp, cfg.monitor_loss != 0);
-    if (fut.valid()) fut.get();
     if (r.bad_pos != ~0ull) {
       const uint64_t jb = r.bad_pos / b;
       k_epoch_restore(c, b, jb);
-      const uint32_t v = cur_perm[r.bad_pos];
+      uint32_t v = 0;
+      F2V_CUDA(cudaMemcpy(&v, c.perm.as<uint32_t>() + r.bad_pos, sizeof(v),
+                          cudaMemcpyDeviceToHost));
       if (failure) {
         failure->epoch = e;
         failure->batch = jb;
@@ -524,6 +509,22 @@ int32_t f2v_partition_epoch(uint32_t n, uint32_t b, uint64_t seed, uint32_t epoc
                             uint32_t* perm_out) {
   return guard(nullptr, [&] {
     partition_epoch(n, b, rng_keyed2(seed, kStreamPartition, epoch), perm_out);
+  });
+}
+
+int32_t f2v_device_partition_epoch(f2v_ctx* h, uint32_t n, uint32_t b, uint64_t seed,
+                                   uint32_t epoch, uint32_t* perm_out) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    F2V_CUDA(cudaSetDevice(c.device));
+    if (b == 0 || b > n) fail(F2V_EUSAGE, "batch size must be in [1, n]");
+    DeviceBuf out;
+    out.ensure(sizeof(uint32_t) * n);
+    k_device_partition(c, n, seed, epoch, out.as<uint32_t>());
+    F2V_CUDA(cudaMemcpyAsync(perm_out, out.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost,
+                             c.stream));
+    F2V_CUDA(cudaStreamSynchronize(c.stream));
+    out.release();
   });
 }
 

@@ -24,6 +24,7 @@ using namespace dev;
 
 constexpr int kWarps = 8;       // warps per CTA
 constexpr int kQ = 64;          // per-warp compaction queue (entries)
+constexpr int kRq = 64;         // per-warp parking lot for the most recent window arcs
 
 struct EpochArgs {
   const uint64_t* rowptr;
@@ -263,40 +264,90 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
   }
 }
 
-// Window arcs of chunks [c0, c1) of u: pass 0 = age > R, pass 1 = age <= R.
+// Take the parked recent window arcs in order, waiting on each row.
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
-__device__ __forceinline__ void window_pass(const EpochArgs& a, uint32_t u, uint32_t j,
-                                            uint32_t c0, uint32_t c1, int pass, int lane,
-                                            uint32_t* qbuf, const float (&zu)[K],
-                                            double (&acc)[K], double& lsum) {
+__device__ __forceinline__ void recent_pass(const EpochArgs& a, int lane, uint32_t* rbuf, int& nr,
+                                            const float (&zu)[K], double (&acc)[K],
+                                            double& lsum) {
+  for (int t0 = 0; t0 < nr; t0 += 32) {
+    const int cnt = min(32, nr - t0);
+    uint32_t pk = 0;
+    if (lane < cnt) {
+      const uint32_t v = rbuf[t0 + lane];
+      wait_written(a.state, v, ld_relaxed(a.state + v));
+      pk = v | kNewBit;
+    }
+    Rows<KIND, K, VEC, MON, FAST>::template run<true>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew,
+                                                      zu, acc, lsum);
+  }
+  __syncwarp();
+  nr = 0;
+}
+
+// Window arcs of chunks [c0, c1) of u.  All chunk counts are fetched at once
+// and the lists walked as one flattened sequence: arcs older than R batches go
+// straight into the row queue; the most recent ones are parked in rbuf and
+// taken last (recent_pass) so the dependency tail of the item is short.  The
+// order is a function of the data only (deterministic).
+template <int KIND, int K, bool VEC, bool MON, bool FAST>
+__device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, uint32_t j,
+                                               uint32_t c0, uint32_t c1, int lane,
+                                               uint32_t* qbuf, uint32_t* rbuf, int& nr,
+                                               const float (&zu)[K], double (&acc)[K],
+                                               double& lsum) {
   const uint64_t r0 = a.rowptr[u];
   const uint32_t cb = a.cbase[u];
   RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0};
-  for (uint32_t c = c0; c < c1; ++c) {
-    const uint32_t m = __ldcg(a.wcnt + cb + c);
-    const uint64_t base = r0 + uint64_t(c) * a.C;
-    for (uint32_t k0 = 0; k0 < m; k0 += 32) {
-      const int cnt = int(umin32(32, m - k0));
-      bool use = false;
-      uint32_t pk = 0;
-      if (lane < cnt) {
-        const uint32_t v = __ldcg(a.wl + base + k0 + lane);
-        const uint32_t st = ld_relaxed(a.state + v);
-        const uint32_t age = j - (st >> 1);
-        use = pass == 0 ? age > a.R : age <= a.R;
-        if (use) {
-          wait_written(a.state, v, st);
-          pk = v | kNewBit;
+  for (uint32_t cc = c0; cc < c1; cc += 32) {
+    const uint32_t nc = umin32(32, c1 - cc);
+    const uint32_t mine = lane < int(nc) ? __ldcg(a.wcnt + cb + cc + lane) : 0u;
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t excl = incl - mine;
+    const uint32_t total = __shfl_sync(kFull, incl, 31);
+    for (uint32_t t0 = 0; t0 < total; t0 += 32) {
+      const uint32_t t = t0 + lane;
+      // chunk of flattened position t: the last chunk whose exclusive start <= t
+      uint32_t ci = 0, off = 0;
+      for (uint32_t i = 0; i < nc; ++i) {
+        const uint32_t e = __shfl_sync(kFull, excl, i);
+        if (e <= t && __shfl_sync(kFull, mine, i) > 0) {
+          ci = i;
+          off = e;
         }
       }
-      q.push(a, lane, use, pk, zu, acc, lsum);
+      bool old = false, recent = false;
+      uint32_t v = 0, st = 0;
+      if (t < total) {
+        v = __ldcg(a.wl + r0 + uint64_t(cc + ci) * a.C + (t - off));
+        st = ld_relaxed(a.state + v);
+        const uint32_t age = j - (st >> 1);
+        old = age > a.R;
+        recent = !old;
+      }
+      if (old) wait_written(a.state, v, st);
+      q.push(a, lane, old, v | kNewBit, zu, acc, lsum);
+      // park the recent ones (processed in place if the parking lot is full)
+      const uint32_t rm = __ballot_sync(kFull, recent);
+      if (nr + __popc(rm) > kRq) {
+        q.flush(a, lane, zu, acc, lsum);
+        recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
+      }
+      if (recent) rbuf[nr + __popc(rm & lanemask_lt(lane))] = v;
+      __syncwarp();
+      nr += __popc(rm);
     }
   }
   q.flush(a, lane, zu, acc, lsum);
 }
 
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
-__device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint32_t* qbuf) {
+__device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint32_t* qbuf,
+                     uint32_t* rbuf) {
   using L = Lay<K, VEC>;
   const uint32_t u = a.perm[p];
   const uint32_t j = p / a.b;
@@ -319,15 +370,17 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   if (nchL == 1) {  // E total + old window arcs + negatives + recent arcs
     L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __ldcg(a.eloss + cb);
-    window_pass<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, 0, lane, qbuf, zu, acc, lsum);
+    int nr = 0;
+    window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
     do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
-    window_pass<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, 1, lane, qbuf, zu, acc, lsum);
+    recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
     finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
     if (lane == 0) a.vflag[u] = 0;
     return;
   }
-  window_pass<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, 0, lane, qbuf, zu, acc, lsum);
-  window_pass<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, 1, lane, qbuf, zu, acc, lsum);
+  int nr = 0;
+  window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
+  recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
   const uint32_t slot = a.lpo[u] + cl;
   L::store_acc(a.lpart + size_t(slot) * a.d, lane, a.d, acc);
   {
@@ -359,9 +412,11 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
 __global__ void __launch_bounds__(kWarps * 32, 2) epoch_kernel(EpochArgs a) {
   __shared__ uint32_t qs[kWarps][kQ];
+  __shared__ uint32_t rs[kWarps][kRq];
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
   uint32_t* qbuf = qs[w];
+  uint32_t* rbuf = rs[w];
   const bool lrole = w >= kWarps - int(a.lwarps);
   uint32_t* counter = a.next + (lrole ? 1 : 0);
   const uint32_t total = lrole ? *a.n_litems : a.n_eitems;
@@ -373,7 +428,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) epoch_kernel(EpochArgs a) {
     uint32_t nxt = 0;
     if (lane == 0) nxt = atomicAdd(counter, 1u);  // claim ahead: hides the atomic's latency
     const uint2 item = items[it];
-    if (lrole) do_L<KIND, K, VEC, MON, FAST>(a, item.x, item.y, lane, qbuf);
+    if (lrole) do_L<KIND, K, VEC, MON, FAST>(a, item.x, item.y, lane, qbuf, rbuf);
     else do_E<KIND, K, VEC, MON, FAST>(a, item.x, item.y, lane, qbuf);
     it = __shfl_sync(kFull, nxt, 0);
   }
@@ -416,16 +471,34 @@ void launch_kind(Ctx& c, const EpochArgs& a, bool mon) {
 void launch_fast_k4(Ctx& c, const EpochArgs& a, bool mon);
 void launch_fast_k2(Ctx& c, const EpochArgs& a, bool mon);
 void launch_fast_k8(Ctx& c, const EpochArgs& a, bool mon);
-void launch_exact_vec(Ctx& c, const EpochArgs& a, bool mon);
-void launch_exact_any(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_vec_k1(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_vec_k2(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_vec_k4(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_vec_k8(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_any_k1(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_any_k2(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_any_k4(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_any_k8(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_any_k16(Ctx& c, const EpochArgs& a, bool mon);
+void launch_exact_any_k32(Ctx& c, const EpochArgs& a, bool mon);
 
 // d = 64/128/256 run FAST when asked; everything else runs EXACT.
 inline void launch_epoch(Ctx& c, const EpochArgs& a, bool mon, bool fast) {
-  if (fast && a.d == 128) launch_fast_k4(c, a, mon);
-  else if (fast && a.d == 64) launch_fast_k2(c, a, mon);
-  else if (fast && a.d == 256) launch_fast_k8(c, a, mon);
-  else if (a.d == 32 || a.d == 64 || a.d == 128 || a.d == 256) launch_exact_vec(c, a, mon);
-  else launch_exact_any(c, a, mon);
+  const uint32_t d = a.d;
+  if (fast && d == 128) launch_fast_k4(c, a, mon);
+  else if (fast && d == 64) launch_fast_k2(c, a, mon);
+  else if (fast && d == 256) launch_fast_k8(c, a, mon);
+  else if (d == 128) launch_exact_vec_k4(c, a, mon);
+  else if (d == 64) launch_exact_vec_k2(c, a, mon);
+  else if (d == 256) launch_exact_vec_k8(c, a, mon);
+  else if (d == 32) launch_exact_vec_k1(c, a, mon);
+  else if (d < 32) launch_exact_any_k1(c, a, mon);
+  else if (d < 64) launch_exact_any_k2(c, a, mon);
+  else if (d < 128) launch_exact_any_k4(c, a, mon);
+  else if (d < 256) launch_exact_any_k8(c, a, mon);
+  else if (d <= 512) launch_exact_any_k16(c, a, mon);
+  else if (d <= 1024) launch_exact_any_k32(c, a, mon);
+  else fail(F2V_EUNSUPPORTED, "dim > 1024 is not supported by the device kernels");
 }
 
 }  // namespace ep

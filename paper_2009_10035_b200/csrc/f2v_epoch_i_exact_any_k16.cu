@@ -1,0 +1,12 @@
+// EXACT-precision epoch kernels, masked layout for d <= 512; the force
+// kind is a run-time parameter.
+#include "f2v_epoch.cuh"
+
+namespace f2v {
+namespace ep {
+void launch_exact_any_k16(Ctx& c, const EpochArgs& a, bool mon) {
+  if (mon) launch_one<-1, 16, false, true, false>(c, a);
+  else launch_one<-1, 16, false, false, false>(c, a);
+}
+}  // namespace ep
+}  // namespace f2v

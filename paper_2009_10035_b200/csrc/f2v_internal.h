@@ -81,6 +81,7 @@ struct Ctx {
       epart, eloss, wcnt, wl, lpart, lloss, ploss, counters;
   uint32_t last_litems = 0;
   DeviceBuf trace;  // DEBUG: per-position finalise timestamps (F2V_TRACE)
+  DeviceBuf shufR, shufL, shufC;  // device Fisher-Yates (f2v_perm.cu)
 
   // timing of the last train_epochs call (f2v_last_timing)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
@@ -106,6 +107,7 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
 EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForceParams& fp,
                         bool monitor);
 void k_epoch_restore(Ctx& c, uint32_t b, uint64_t bad_batch);
+void k_device_partition(Ctx& c, uint32_t n, uint64_t seed, uint32_t epoch, uint32_t* perm_out);
 
 ForceParams make_params(const f2v_force_model& m);
 
