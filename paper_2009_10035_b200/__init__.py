@@ -28,7 +28,9 @@ __all__ = [
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "lib", "libf2v_b200.so")
+# F2V_LIB selects another build of the same library (e.g. the device-checks
+# debug build, lib/libf2v_b200_dbg.so); default is the release build.
+_LIB_PATH = os.environ.get("F2V_LIB") or os.path.join(_PKG, "lib", "libf2v_b200.so")
 
 
 def lib_path() -> str:

@@ -34,6 +34,12 @@ void cuda_check(cudaError_t e, const char* what) {
     fail(F2V_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e) + " at " + what);
 }
 
+void launch_check(cudaStream_t s, const char* what) {
+  cuda_check(cudaGetLastError(), what);
+  static const bool sync = std::getenv("F2V_SYNC_DEBUG") != nullptr;
+  if (sync) cuda_check(cudaStreamSynchronize(s), what);
+}
+
 void DeviceBuf::ensure(size_t want) {
   if (want <= bytes && p) return;
   release();

@@ -240,21 +240,21 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
                                                          c.state.as<uint32_t>(), n, b,
                                                          c.cbase.as<uint32_t>(),
                                                          c.nE.as<uint32_t>(), c.wtot.as<uint32_t>());
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "state_kernel");
   negs_kernel<<<(nb + 255) / 256, 256, 0, c.stream>>>(
       c.negs_all.as<uint32_t>(), c.negwin.as<uint32_t>(), c.state.as<uint32_t>(), nb, s, n, seed,
       epoch, sampler, W);
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "negs_kernel");
   window_scan_kernel<<<uint32_t((c.chunks * 32 + 255) / 256), 256, 0, c.stream>>>(
       c.rowptr.as<uint64_t>(), c.col.as<uint32_t>(), c.cvert.as<uint32_t>(),
       c.cbase.as<uint32_t>(), c.state.as<uint32_t>(), c.wtot.as<uint32_t>(), c.chunks,
       c.tune.chunk, W);
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "window_scan_kernel");
   needs_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
       c.perm.as<uint32_t>(), n, b, c.wtot.as<uint32_t>(), c.negwin.as<uint32_t>(),
       c.lbase.as<uint32_t>(), c.needs.as<uint32_t>(), c.nL.as<uint32_t>(),
       std::getenv("F2V_DEBUG_NODEP") ? 1 : 0);
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "needs_kernel");
   size_t tmp = 0;
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.nE.as<uint32_t>(), c.EP.as<uint32_t>(),
                                          n + 1, c.stream));
@@ -265,10 +265,10 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
                                          c.LP.as<uint32_t>(), n + 1, c.stream));
   emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.EP.as<uint32_t>(), c.nE.as<uint32_t>(),
                                                      c.items.as<uint2>(), n);
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "emit_kernel");
   emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.LP.as<uint32_t>(), c.nL.as<uint32_t>(),
                                                      c.litems.as<uint2>(), n);
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "emit_kernel");
   // number of L items (device value, read back asynchronously with the run)
   F2V_CUDA(cudaMemcpyAsync(c.counters.as<uint32_t>() + 8, c.LP.as<uint32_t>() + n,
                            sizeof(uint32_t), cudaMemcpyDeviceToDevice, c.stream));
@@ -323,6 +323,9 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.eta = eta;
   a.fp = fp;
   a.nodep = std::getenv("F2V_DEBUG_NODEP") ? 1 : 0;
+  a.nnz = c.nnz;
+  a.chunks = c.chunks;
+  a.lslots = c.lslots;
   a.trace = nullptr;
   if (std::getenv("F2V_TRACE")) {
     c.trace.ensure(sizeof(unsigned long long) * std::max<uint32_t>(c.n, 1));
@@ -339,7 +342,7 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   if (monitor) {
     sum_kernel<<<1, 1024, 0, c.stream>>>(c.ploss.as<double>(), c.n,
                                          reinterpret_cast<double*>(ctr + 4));
-    F2V_CUDA(cudaGetLastError());
+    F2V_LAUNCHED(c.stream, "sum_kernel");
     ++c.launches;
   }
   uint64_t host[5];
@@ -361,7 +364,7 @@ void k_epoch_restore(Ctx& c, uint32_t b, uint64_t bad_batch) {
   const uint64_t total = uint64_t(c.n) * c.d;
   restore_kernel<<<uint32_t((total + 255) / 256), 256, 0, c.stream>>>(
       c.state.as<uint32_t>(), c.z[1 - c.cur].as<float>(), c.zcur(), c.n, c.d, bad_batch);
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "restore_kernel");
   ++c.launches;
   F2V_CUDA(cudaStreamSynchronize(c.stream));
 }

@@ -59,6 +59,7 @@ struct EpochArgs {
   uint32_t C, G, W, R, lwarps;
   float eta;
   ForceParams fp;
+  uint64_t nnz, chunks, lslots;  // bounds, used by F2V_DEVICE_CHECKS builds
   int nodep;                    // DEBUG (F2V_DEBUG_NODEP): every row read from Zold, no waits
   unsigned long long* trace;    // DEBUG (F2V_TRACE): per position finalise time (ns)
 };
@@ -68,6 +69,22 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+
+#ifdef F2V_DEVICE_CHECKS
+#define DCHECK(cond, ...)                                                      \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      printf("F2V_DEVICE_CHECK %s:%d " #cond " | ", __FILE__, __LINE__);      \
+      printf(__VA_ARGS__);                                                     \
+      printf("\n");                                                           \
+      __trap();                                                                \
+    }                                                                          \
+  } while (0)
+#else
+#define DCHECK(cond, ...) \
+  do {                    \
+  } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t wait_written(const uint32_t* state, uint32_t v, uint32_t st) {
   while (!(st & 1u)) {
@@ -170,12 +187,16 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
 __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint32_t* qbuf) {
   using L = Lay<K, VEC>;
+  DCHECK(p < a.n, "E p=%u n=%u", p, a.n);
   const uint32_t u = a.perm[p];
+  DCHECK(u < a.n, "E u=%u", u);
   const uint32_t j = p / a.b;
   const uint64_t r0 = a.rowptr[u], r1 = a.rowptr[u + 1];
   const uint32_t cb = a.cbase[u];
   const uint32_t nch = a.cbase[u + 1] - cb;
   const uint32_t cs = cb + c;
+  DCHECK(c < nch && cs < a.chunks, "E c=%u nch=%u cs=%u chunks=%llu", c, nch, cs,
+         (unsigned long long)a.chunks);
   const uint64_t e0 = r0 + uint64_t(c) * a.C;
   const uint64_t e1 = umin64(e0 + a.C, r1);
   float zu[K];
@@ -191,7 +212,10 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
     uint32_t v = 0, pk = 0;
     bool use = false, win = false;
     if (lane < cnt) {
+      DCHECK(e + lane < a.nnz, "E arc %llu nnz %llu", (unsigned long long)(e + lane),
+             (unsigned long long)a.nnz);
       v = a.col[e + lane];
+      DCHECK(v < a.n, "E v=%u", v);
       const uint32_t st = ld_relaxed(a.state + v);
       const uint32_t bv = st >> 1;
       if (bv >= j || a.nodep) {
@@ -206,6 +230,7 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
       }
     }
     const uint32_t wm = __ballot_sync(kFull, win);
+    DCHECK(!win || e0 + wc + __popc(wm & lanemask_lt(lane)) < e1, "E wl overflow");
     if (win) a.wl[e0 + wc + __popc(wm & lanemask_lt(lane))] = v;
     wc += __popc(wm);
     q.push(a, lane, use, pk, zu, acc, lsum);
@@ -313,9 +338,10 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, u
       const uint32_t t = t0 + lane;
       // chunk of flattened position t: the last chunk whose exclusive start <= t
       uint32_t ci = 0, off = 0;
-      for (uint32_t i = 0; i < nc; ++i) {
+      for (uint32_t i = 0; i < nc; ++i) {  // shuffles outside any lane-divergent branch
         const uint32_t e = __shfl_sync(kFull, excl, i);
-        if (e <= t && __shfl_sync(kFull, mine, i) > 0) {
+        const uint32_t m = __shfl_sync(kFull, mine, i);
+        if (e <= t && m > 0) {
           ci = i;
           off = e;
         }
@@ -323,7 +349,10 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, u
       bool old = false, recent = false;
       uint32_t v = 0, st = 0;
       if (t < total) {
+        DCHECK(cc + ci < c1 && t - off < a.C && r0 + uint64_t(cc + ci) * a.C + (t - off) < a.nnz,
+               "L wl t=%u off=%u ci=%u cc=%u c1=%u", t, off, ci, cc, c1);
         v = __ldcg(a.wl + r0 + uint64_t(cc + ci) * a.C + (t - off));
+        DCHECK(v < a.n, "L wl v=%u", v);
         st = ld_relaxed(a.state + v);
         const uint32_t age = j - (st >> 1);
         old = age > a.R;
@@ -349,7 +378,9 @@ template <int KIND, int K, bool VEC, bool MON, bool FAST>
 __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint32_t* qbuf,
                      uint32_t* rbuf) {
   using L = Lay<K, VEC>;
+  DCHECK(p < a.n, "L p=%u", p);
   const uint32_t u = a.perm[p];
+  DCHECK(u < a.n, "L u=%u", u);
   const uint32_t j = p / a.b;
   const uint32_t cb = a.cbase[u];
   const uint32_t nch = a.cbase[u + 1] - cb;
@@ -382,6 +413,8 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
   recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
   const uint32_t slot = a.lpo[u] + cl;
+  DCHECK(slot < a.lslots, "L slot=%u lslots=%llu cl=%u nchL=%u", slot,
+         (unsigned long long)a.lslots, cl, nchL);
   L::store_acc(a.lpart + size_t(slot) * a.d, lane, a.d, acc);
   {
     const double ls = MON ? warp_sum_d(lsum) : 0.0;
@@ -425,6 +458,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) epoch_kernel(EpochArgs a) {
   if (lane == 0) it = atomicAdd(counter, 1u);
   it = __shfl_sync(kFull, it, 0);
   while (it < total) {
+    DCHECK(it < (lrole ? a.chunks + a.lslots + a.n : a.chunks), "item %u", it);
     uint32_t nxt = 0;
     if (lane == 0) nxt = atomicAdd(counter, 1u);  // claim ahead: hides the atomic's latency
     const uint2 item = items[it];
@@ -446,7 +480,7 @@ void launch_one(Ctx& c, const EpochArgs& a) {
   const uint32_t need = uint32_t(std::max<uint64_t>((a.n_eitems + ew - 1) / ew, 1));
   blocks = std::max(1u, std::min(blocks, need));
   kern<<<blocks, kWarps * 32, 0, c.stream>>>(a);
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "kern");
   ++c.launches;
 }
 

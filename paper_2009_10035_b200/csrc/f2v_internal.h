@@ -20,6 +20,10 @@ struct Error {
 [[noreturn]] void fail(int32_t code, const std::string& msg);
 void cuda_check(cudaError_t e, const char* what);
 #define F2V_CUDA(x) ::f2v::cuda_check((x), #x)
+// after a launch: launch errors always; with F2V_SYNC_DEBUG=1 also synchronise
+// so an asynchronous fault is attributed to the kernel that caused it.
+void launch_check(cudaStream_t s, const char* what);
+#define F2V_LAUNCHED(stream, name) ::f2v::launch_check((stream), (name))
 
 // Per-pair model parameters in the form the kernels use.
 struct ForceParams {

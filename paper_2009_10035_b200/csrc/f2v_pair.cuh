@@ -20,6 +20,7 @@ namespace f2v {
 namespace dev {
 
 constexpr unsigned kFull = 0xffffffffu;
+
 constexpr uint32_t kNewBit = 0x80000000u;
 
 // Relaxed (no L1 invalidation) global loads/stores for cross-warp flags; the

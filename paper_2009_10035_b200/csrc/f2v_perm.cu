@@ -106,6 +106,7 @@ void k_device_partition(Ctx& c, uint32_t n, uint64_t seed, uint32_t epoch, uint3
   const int blocks = std::max(1, per_sm) * c.num_sms;
   void* args[] = {&a};
   F2V_CUDA(cudaLaunchCooperativeKernel((void*)shuffle_kernel, blocks, 256, args, 0, c.stream));
+  F2V_LAUNCHED(c.stream, "shuffle_kernel");
   ++c.launches;
 }
 

@@ -110,7 +110,7 @@ void launch_step(Ctx& c, const StepArgs& a, uint32_t blocks) {
   else if (d <= 256) grad_step_kernel<8, false, MON><<<blocks, 256, 0, st>>>(a);
   else if (d <= 512) grad_step_kernel<16, false, MON><<<blocks, 256, 0, st>>>(a);
   else grad_step_kernel<32, false, MON><<<blocks, 256, 0, st>>>(a);
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "kernel");
   ++c.launches;
 }
 
@@ -171,14 +171,14 @@ void k_apply_update(Ctx& c, uint32_t b, float eta, bool unique_ids) {
     apply_seq_kernel<<<(c.d + 127) / 128, 128, 0, c.stream>>>(c.zcur(), c.ids.as<uint32_t>(),
                                                                c.grads.as<float>(), b, c.d, eta);
   }
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "apply_seq_kernel");
   ++c.launches;
 }
 
 double k_batch_loss_sum(Ctx& c, uint32_t b) {
   c.scratch.ensure(sizeof(double));
   sum_kernel<<<1, 1024, 0, c.stream>>>(c.vloss.as<double>(), b, c.scratch.as<double>());
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "sum_kernel");
   ++c.launches;
   double out = 0.0;
   F2V_CUDA(cudaMemcpyAsync(&out, c.scratch.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
@@ -203,7 +203,7 @@ void k_uniform_embedding(Ctx& c, uint64_t seed, float lo, float hi, int keyed_in
   if (total == 0) return;
   uniform_kernel<<<uint32_t((total + 255) / 256), 256, 0, c.stream>>>(c.zcur(), total, s0, dlo,
                                                                      dhi);
-  F2V_CUDA(cudaGetLastError());
+  F2V_LAUNCHED(c.stream, "uniform_kernel");
   ++c.launches;
 }
 
