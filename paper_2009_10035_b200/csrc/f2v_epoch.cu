@@ -126,6 +126,19 @@ __global__ void negs_kernel(uint32_t* __restrict__ out, uint32_t* __restrict__ n
   negwin[j] = win;
 }
 
+// Znew := the sentinel NaN everywhere (rows become readable once stored).
+__global__ void sentinel_kernel(uint4* __restrict__ z, uint64_t n16) {
+  const uint4 s = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    __stcg(z + i, s);
+}
+
+__global__ void sentinel_tail_kernel(float* __restrict__ z, uint64_t from, uint64_t to) {
+  const uint64_t i = from + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < to) z[i] = __uint_as_float(kSentinel);
+}
+
 // On a NumericalError at batch jb: rows of batches >= jb go back to Zold so
 // Znew is the state after the last complete batch (trainer.cpp:149-152).
 __global__ void restore_kernel(const uint32_t* __restrict__ state, const float* __restrict__ zold,
@@ -282,6 +295,15 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   uint32_t* ctr = c.counters.as<uint32_t>();  // [0..1] claims, [2..3] bad, [4..5] loss, [8] nL
   F2V_CUDA(cudaMemsetAsync(ctr, 0, 8, c.stream));
   F2V_CUDA(cudaMemsetAsync(ctr + 2, 0xff, 8, c.stream));
+  {  // Znew := sentinel (cudaMalloc'd buffers are 256-byte aligned)
+    const uint64_t total = uint64_t(c.n) * c.d, n16 = total / 4;
+    sentinel_kernel<<<uint32_t(std::min<uint64_t>((n16 + 255) / 256, 4u * c.num_sms * 8)), 256, 0,
+                      c.stream>>>(c.z[nxt].as<uint4>(), n16);
+    F2V_LAUNCHED(c.stream, "sentinel_kernel");
+    if (total % 4)
+      sentinel_tail_kernel<<<1, 4, 0, c.stream>>>(c.z[nxt].as<float>(), n16 * 4, total);
+    c.launches += 1;
+  }
   ep::EpochArgs a;
   a.rowptr = c.rowptr.as<uint64_t>();
   a.col = c.col.as<uint32_t>();
@@ -327,9 +349,12 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.chunks = c.chunks;
   a.lslots = c.lslots;
   a.trace = nullptr;
+  a.ltrace = nullptr;
   if (std::getenv("F2V_TRACE")) {
-    c.trace.ensure(sizeof(unsigned long long) * std::max<uint32_t>(c.n, 1));
+    c.trace.ensure(sizeof(unsigned long long) * 5 * std::max<uint32_t>(c.n, 1));
     a.trace = c.trace.as<unsigned long long>();
+    a.ltrace = a.trace + c.n;
+    F2V_CUDA(cudaMemsetAsync(a.ltrace, 0, sizeof(unsigned long long) * 4 * c.n, c.stream));
   }
   if (!c.ev_kernel.size()) {
     c.ev_kernel.resize(2);

@@ -62,6 +62,7 @@ struct EpochArgs {
   uint64_t nnz, chunks, lslots;  // bounds, used by F2V_DEVICE_CHECKS builds
   int nodep;                    // DEBUG (F2V_DEBUG_NODEP): every row read from Zold, no waits
   unsigned long long* trace;    // DEBUG (F2V_TRACE): per position finalise time (ns)
+  unsigned long long* ltrace;   // DEBUG (F2V_TRACE): per position L-item stage times (4 x ns)
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -85,14 +86,6 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   do {                    \
   } while (0)
 #endif
-
-__device__ __forceinline__ uint32_t wait_written(const uint32_t* state, uint32_t v, uint32_t st) {
-  while (!(st & 1u)) {
-    __nanosleep(32);
-    st = ld_relaxed(state + v);
-  }
-  return st;
-}
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
@@ -143,8 +136,7 @@ __device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, int
       const uint32_t w = a.negs[size_t(j) * a.s + k0 + lane];
       const uint32_t st = ld_relaxed(a.state + w);
       if ((st >> 1) < j && !a.nodep) {
-        wait_written(a.state, w, st);
-        pk = w | kNewBit;
+        pk = w | kNewBit;  // Znew row: the row loads poll its sentinel
       } else {
         pk = w;
       }
@@ -168,18 +160,16 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_
     const float g = __double2float_rn(acc[k]);
     if (L::valid(lane, k, a.d) && !isfinite(g)) bad = true;
     nz[k] = __fsub_rn(zu[k], __fmul_rn(a.eta, g));
+    if (nz[k] != nz[k]) nz[k] = __int_as_float(0x7fffffff);  // never the sentinel NaN
   }
-  L::store(a.znew + size_t(u) * a.d, lane, a.d, nz);
+  L::store(a.znew + size_t(u) * a.d, lane, a.d, nz);  // publishes the row (sentinel-free)
   const bool any_bad = __any_sync(kFull, bad);
   if (MON) {
     const double tot = warp_sum_d(lsum);
     if (lane == 0) a.ploss[p] = tot;
   }
-  __threadfence();
-  __syncwarp();
   if (lane == 0) {
     if (any_bad) atomicMin(a.bad, (unsigned long long)p);
-    atomicOr(a.state + u, 1u);
     if (a.trace) a.trace[p] = globaltimer();
   }
 }
@@ -221,8 +211,7 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
       if (bv >= j || a.nodep) {
         use = true;
         pk = v;
-      } else if (bv + a.W < j) {  // past: final long ago (rarely waits)
-        wait_written(a.state, v, st);
+      } else if (bv + a.W < j) {  // past: final long ago (the row load rarely polls)
         use = true;
         pk = v | kNewBit;
       } else {
@@ -299,7 +288,6 @@ __device__ __forceinline__ void recent_pass(const EpochArgs& a, int lane, uint32
     uint32_t pk = 0;
     if (lane < cnt) {
       const uint32_t v = rbuf[t0 + lane];
-      wait_written(a.state, v, ld_relaxed(a.state + v));
       pk = v | kNewBit;
     }
     Rows<KIND, K, VEC, MON, FAST>::template run<true>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew,
@@ -358,7 +346,6 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, u
         old = age > a.R;
         recent = !old;
       }
-      if (old) wait_written(a.state, v, st);
       q.push(a, lane, old, v | kNewBit, zu, acc, lsum);
       // park the recent ones (processed in place if the parking lot is full)
       const uint32_t rm = __ballot_sync(kFull, recent);
@@ -385,6 +372,8 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   const uint32_t cb = a.cbase[u];
   const uint32_t nch = a.cbase[u + 1] - cb;
   const uint32_t nchL = a.lbase[u + 1] - a.lbase[u];
+  unsigned long long* lt = (a.ltrace && cl == 0) ? a.ltrace + 4ull * p : nullptr;
+  if (lt && lane == 0) lt[0] = globaltimer();
   float zu[K];
   L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
   double acc[K];
@@ -397,6 +386,7 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     __nanosleep(64);
     f = ld_relaxed(a.vflag + u);
   }
+  if (lt && lane == 0) lt[1] = globaltimer();
   const uint32_t c0 = cl * a.G, c1 = umin32(nch, c0 + a.G);
   if (nchL == 1) {  // E total + old window arcs + negatives + recent arcs
     L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
@@ -404,7 +394,9 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     int nr = 0;
     window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
     do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+    if (lt && lane == 0) lt[2] = globaltimer();
     recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
+    if (lt && lane == 0) lt[3] = globaltimer();
     finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
     if (lane == 0) a.vflag[u] = 0;
     return;

@@ -23,6 +23,19 @@ constexpr unsigned kFull = 0xffffffffu;
 
 constexpr uint32_t kNewBit = 0x80000000u;
 
+// Znew rows hold this NaN bit pattern until their final value is stored: a
+// reader polls the row itself instead of a separate flag (one L2 round trip,
+// no fence on the writer).  Finalised values are never this NaN.
+constexpr uint32_t kSentinel = 0xffc0ffeeu;
+
+template <int K>
+__device__ __forceinline__ bool has_sentinel(const float (&v)[K]) {
+  bool b = false;
+#pragma unroll
+  for (int k = 0; k < K; ++k) b |= __float_as_uint(v[k]) == kSentinel;
+  return b;
+}
+
 // Relaxed (no L1 invalidation) global loads/stores for cross-warp flags; the
 // data they guard is always read through L2 (ld.cg) after the flag is seen.
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
@@ -76,6 +89,14 @@ struct Lay {
         const uint32_t c = col(lane, k);
         v[k] = (VEC || c < d) ? (coherent ? __ldcg(row + c) : __ldg(row + c)) : 0.0f;
       }
+    }
+  }
+  // a Znew row: re-load until no lane sees the sentinel (warp-uniform loop)
+  __device__ static __forceinline__ void poll(const float* row, int lane, uint32_t d,
+                                              float (&v)[K]) {
+    while (__any_sync(kFull, has_sentinel<K>(v))) {
+      __nanosleep(20);
+      load(row, lane, d, v, true);
     }
   }
   __device__ static __forceinline__ void store(float* row, int lane, uint32_t d,
@@ -251,6 +272,12 @@ __device__ __forceinline__ void rows_exact(const ForceParams& fp, uint32_t packe
         for (int k = 0; k < K; ++k) v[i][k] = 0.0f;
       }
     }
+#pragma unroll
+    for (int i = 0; i < U; ++i) {  // Znew rows not yet final: poll
+      const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
+      if (k0 + i < cnt && (pk & kNewBit))
+        L::poll(znew + size_t(pk & ~kNewBit) * d, lane, d, v[i]);
+    }
     double w[U][K], red[U], nw[U];
 #pragma unroll
     for (int i = 0; i < U; ++i) {
@@ -410,6 +437,12 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
 #pragma unroll
         for (int k = 0; k < K; ++k) w[i][k] = 0.0f;
       }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {  // Znew rows not yet final: poll
+      const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
+      if (k0 + i < cnt && (pk & kNewBit))
+        L::poll(znew + size_t(pk & ~kNewBit) * d, lane, d, w[i]);
     }
     float part[8], nrm[8];
 #pragma unroll

@@ -15,19 +15,38 @@ cfg = f2v.TrainConfig(dim=128, batch=b, negatives=5, lr=0.02, epochs=4,
 for e in range(3):
     dev.train_epochs(cfg, e, 1)
     t = dev.last_timing()
-tr = np.zeros(n, np.uint64); nl = C.c_uint32()
+tr = np.zeros(5 * n, np.uint64); nl = C.c_uint32()
 lib.f2v_debug_trace(dev._h, tr, C.byref(nl))
-t0 = tr.min(); tr = (tr - t0) / 1e3  # us
+fin = tr[:n].astype(np.float64); lt = tr[n:].reshape(n, 4).astype(np.float64)
+t0 = fin.min(); fin = (fin - t0) / 1e3
+has = lt[:, 0] > 0
+lt[has] = (lt[has] - t0) / 1e3
 nb = (n + b - 1) // b
-bt = np.array([tr[i*b:(i+1)*b].max() for i in range(nb)])
-deg = g.degrees(); perm = f2v.partition_epoch(n, b, 1, 2)
-print(json.dumps({"kernel_ms": t["epoch_kernel_ms"], "device_ms": t["device_ms"], "litems": nl.value,
-      "batch_done_us_pctl": [float(np.percentile(bt, q)) for q in (1, 10, 25, 50, 75, 90, 99, 100)]}))
+bt = np.array([fin[i*b:(i+1)*b].max() for i in range(nb)])
+print(json.dumps({"kernel_ms": t["epoch_kernel_ms"], "device_ms": t["device_ms"], "litems": nl.value}))
 d = np.diff(np.maximum.accumulate(bt))
 print("per-batch frontier advance us: mean %.2f median %.2f p90 %.2f p99 %.2f max %.1f" % (d.mean(), np.median(d), np.percentile(d,90), np.percentile(d,99), d.max()))
-slow = np.argsort(-d)[:10]
-for i in slow:
-    ids = perm[(i+1)*b:(i+2)*b]
-    print("batch", i+1, "advance %.1f us" % d[i], "maxdeg in batch", int(deg[ids].max()) if len(ids) else 0)
-for q in range(0, nb, nb // 20):
-    print(q, "%.0f" % bt[q])
+# critical vertex per batch = last finaliser; its L stages
+crit = np.array([i*b + int(np.argmax(fin[i*b:(i+1)*b])) for i in range(nb)])
+cl = crit[has[crit]]
+print("critical vertices with an L item: %d of %d" % (len(cl), nb))
+prev_done = np.concatenate([[0], np.maximum.accumulate(bt)[:-1]])[cl // b]
+st = lt[cl]
+print("L claim - prev batch done (us): median %.2f" % np.median(st[:, 0] - prev_done))
+print("E wait (vflag) us: median %.2f p90 %.2f" % (np.median(st[:, 1] - st[:, 0]), np.percentile(st[:, 1] - st[:, 0], 90)))
+print("old+negs us: median %.2f p90 %.2f" % (np.median(st[:, 2] - st[:, 1]), np.percentile(st[:, 2] - st[:, 1], 90)))
+print("recent wait us: median %.2f p90 %.2f" % (np.median(st[:, 3] - st[:, 2]), np.percentile(st[:, 3] - st[:, 2], 90)))
+print("recent done - prev batch done: median %.2f" % np.median(st[:, 3] - prev_done))
+print("finalize tail us (final - recent done): median %.2f p90 %.2f" % (np.median(fin[cl] - st[:, 3]), np.percentile(fin[cl] - st[:, 3], 90)))
+print("final - prev batch done: median %.2f" % np.median(fin[cl] - prev_done))
+deg = g.degrees(); perm = dev.partition_epoch(n, b, 1, 2)
+print("critical deg median", np.median(deg[perm[crit]]), "p90", np.percentile(deg[perm[crit]], 90))
+ok = (lt[cl, 2] > 0) & (lt[cl, 3] > 0)
+c2 = cl[ok]; pd = prev_done[ok]
+def pc(x): return "median %.2f p25 %.2f p75 %.2f p90 %.2f" % (np.median(x), np.percentile(x, 25), np.percentile(x, 75), np.percentile(x, 90))
+print("n crit with full L trace", len(c2))
+print("vflag seen - prev_done:", pc(lt[c2, 1] - pd))
+print("old+negs done - prev_done:", pc(lt[c2, 2] - pd))
+print("recent done - prev_done:", pc(lt[c2, 3] - pd))
+print("final - prev_done:", pc(fin[c2] - pd))
+print("final - recent done:", pc(fin[c2] - lt[c2, 3]))
