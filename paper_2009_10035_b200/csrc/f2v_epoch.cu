@@ -76,9 +76,15 @@ __global__ void window_scan_kernel(const uint64_t* __restrict__ rowptr,
   const uint64_t r0 = rowptr[u], r1 = rowptr[u + 1];
   const uint64_t e0 = r0 + uint64_t(cs - cbase[u]) * C, e1 = umin64(e0 + C, r1);
   uint32_t cnt = 0;
-  for (uint64_t e = e0 + lane; e < e1; e += 32) {
-    const uint32_t bv = state[col[e]] >> 1;
-    cnt += (bv < j && bv + W >= j) ? 1u : 0u;
+  for (uint64_t e = e0 + lane; e < e1; e += 32 * 8) {  // 8 independent gathers in flight
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = e + 32 * i < e1 ? __ldg(col + e + 32 * i) : 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t bv = __ldg(state + v[i]) >> 1;
+      cnt += (e + 32 * i < e1 && bv < j && bv + W >= j) ? 1u : 0u;
+    }
   }
 #pragma unroll
   for (int m = 16; m; m >>= 1) cnt += __shfl_xor_sync(kFull, cnt, m);

@@ -85,7 +85,7 @@ struct Ctx {
       epart, eloss, wcnt, wl, lpart, lloss, ploss, counters;
   uint32_t last_litems = 0;
   DeviceBuf trace;  // DEBUG: per-position finalise timestamps (F2V_TRACE)
-  DeviceBuf shufR, shufL, shufC;  // device Fisher-Yates (f2v_perm.cu)
+  DeviceBuf shufR, shufL;  // device Fisher-Yates (f2v_perm.cu)
 
   // timing of the last train_epochs call (f2v_last_timing)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;

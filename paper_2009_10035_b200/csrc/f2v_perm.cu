@@ -4,110 +4,129 @@
 // The reference performs, for m = n-1 down to 1, swap(A[m], A[J_m]) with
 // J_m = below(m + 1) from draw number n-1-m of the keyed SplitMix stream
 // (seed, {0x22, epoch}).  Every J_m is known up front (counter-based stream),
-// so the swaps can run as "deterministic reservations" (Shun, Gu, Blelloch,
-// Fineman, Gibbons, SODA'15): in each round every pending step m reserves
-// both positions it touches with priority m (an atomicMax of a round-stamped
-// key); a step whose reservations both survive commits its swap.  A step
-// commits only when every earlier (larger-m) step touching its positions has
-// committed, and steps committing in one round touch disjoint positions, so
-// each swap sees exactly the array state the sequential loop gives it.  The
-// dependence depth is O(log n) w.h.p.; the rounds run inside one cooperative
-// kernel with a grid barrier between the reserve and commit phases.
-#include <cooperative_groups.h>
+// so the final array has a closed form:
+//   position m is final right after step m, so A[m] = V(J_m, m), the value at
+//   position J_m just before step m.  That position was last written by the
+//   smallest step m' > m with J_m' = J_m (which moved in W(m'), the value at
+//   position m' just before step m'), or never (value J_m).  Likewise
+//   W(m) = W(next(m)) with next(m) = the smallest step m'' > m targeting m,
+//   and W(m) = m when there is none.
+// Steps are grouped by target with a stable radix sort of (J_m, m); the W
+// chains (strictly increasing step indices) are resolved by pointer jumping.
+// O(n log n) work, ~log2(n) short passes, no sequential loop.
+#include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
 
 #include "f2v_internal.h"
 #include "f2v_rng.h"
 
-namespace cg = cooperative_groups;
-
 namespace f2v {
 namespace {
 
-struct ShuffleArgs {
-  uint32_t* A;                 // the permutation, initialised to iota
-  unsigned long long* R;       // reservations, zeroed
-  uint32_t* list[2];           // pending step lists (ping-pong)
-  uint32_t* count;             // [0], [1]: pending counts; [2] rounds used
-  uint32_t n;
-  uint64_t s0;                 // keyed stream state
-};
+constexpr uint32_t kNone = 0xffffffffu;
 
-__device__ __forceinline__ uint32_t target(const ShuffleArgs& a, uint32_t m) {
-  return uint32_t(rng_below(rng_draw(a.s0, uint64_t(a.n) - 1 - m), uint64_t(m) + 1));
+__global__ void targets_kernel(uint32_t* __restrict__ key, uint32_t* __restrict__ val, uint32_t n,
+                               uint64_t s0) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;  // step m = i + 1
+  if (i + 1 >= n) return;
+  const uint32_t m = i + 1;
+  key[i] = uint32_t(rng_below(rng_draw(s0, uint64_t(n) - 1 - m), uint64_t(m) + 1));
+  val[i] = m;
 }
 
-__global__ void shuffle_kernel(ShuffleArgs a) {
-  cg::grid_group grid = cg::this_grid();
-  const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
-  // init: A = iota, R = 0, all steps m in [1, n) pending
-  for (uint64_t i = tid; i < a.n; i += stride) {
-    __stcg(a.A + i, uint32_t(i));
-    __stcg(a.R + i, 0ull);
-    if (i >= 1) __stcg(a.list[0] + i - 1, uint32_t(i));
+// sorted (J, m): successor of m inside its target group, first step of each group
+__global__ void groups_kernel(const uint32_t* __restrict__ ks, const uint32_t* __restrict__ vs,
+                              uint32_t N, uint32_t* __restrict__ succ,
+                              uint32_t* __restrict__ first) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const uint32_t key = ks[k], m = vs[k];
+  succ[m] = (k + 1 < N && ks[k + 1] == key) ? vs[k + 1] : kNone;
+  if (k == 0 || ks[k - 1] != key) first[key] = m;
+}
+
+// next(m): the smallest step > m targeting m (root: itself)
+__global__ void next_kernel(const uint32_t* __restrict__ succ, const uint32_t* __restrict__ first,
+                            uint32_t* __restrict__ ptr, uint32_t n) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  if (m == 0) {
+    ptr[0] = 0;
+    return;
   }
-  if (tid == 0) {
-    a.count[0] = a.n > 0 ? a.n - 1 : 0;
-    a.count[1] = 0;
+  uint32_t f = first[m];
+  if (f == m) f = succ[m];  // J_m == m: skip the self-target
+  ptr[m] = f == kNone ? m : f;
+}
+
+__global__ void jump_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                            uint32_t n) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m < n) out[m] = in[in[m]];
+}
+
+__global__ void final_kernel(const uint32_t* __restrict__ succ, const uint32_t* __restrict__ first,
+                             const uint32_t* __restrict__ W, uint32_t* __restrict__ A, uint32_t n,
+                             uint64_t s0) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  if (m == 0) {
+    const uint32_t f = first[0];
+    A[0] = f == kNone ? 0u : W[f];
+    return;
   }
-  grid.sync();
-  uint32_t round = 1;
-  int cur = 0;
-  while (true) {
-    const uint32_t pending = __ldcg(a.count + cur);
-    if (pending == 0) break;
-    const unsigned long long stamp = (unsigned long long)round << 32;
-    for (uint64_t t = tid; t < pending; t += stride) {  // reserve
-      const uint32_t m = __ldcg(a.list[cur] + t);
-      const uint32_t J = target(a, m);
-      atomicMax(a.R + m, stamp | m);
-      if (J != m) atomicMax(a.R + J, stamp | m);
-    }
-    if (tid == 0) a.count[cur ^ 1] = 0;
-    grid.sync();
-    for (uint64_t t = tid; t < pending; t += stride) {  // commit or defer
-      const uint32_t m = __ldcg(a.list[cur] + t);
-      const uint32_t J = target(a, m);
-      const unsigned long long key = stamp | m;
-      if (__ldcg(a.R + m) == key && __ldcg(a.R + J) == key) {
-        const uint32_t x = __ldcg(a.A + m);
-        __stcg(a.A + m, __ldcg(a.A + J));
-        __stcg(a.A + J, x);
-      } else {
-        __stcg(a.list[cur ^ 1] + atomicAdd(a.count + (cur ^ 1), 1u), m);
-      }
-    }
-    grid.sync();
-    cur ^= 1;
-    ++round;
-  }
-  if (tid == 0) a.count[2] = round - 1;
+  const uint32_t s = succ[m];
+  A[m] = s != kNone ? W[s]
+                    : uint32_t(rng_below(rng_draw(s0, uint64_t(n) - 1 - m), uint64_t(m) + 1));
 }
 
 }  // namespace
 
 // perm_out (device, n entries) = partition_epoch(n, b, Rng::keyed(seed, {0x22, epoch})).perm
 void k_device_partition(Ctx& c, uint32_t n, uint64_t seed, uint32_t epoch, uint32_t* perm_out) {
-  c.shufR.ensure(sizeof(unsigned long long) * std::max<uint32_t>(n, 1));
-  c.shufL.ensure(sizeof(uint32_t) * 2 * std::max<uint32_t>(n, 1));
-  c.shufC.ensure(sizeof(uint32_t) * 4);
-  ShuffleArgs a;
-  a.A = perm_out;
-  a.R = c.shufR.as<unsigned long long>();
-  a.list[0] = c.shufL.as<uint32_t>();
-  a.list[1] = c.shufL.as<uint32_t>() + std::max<uint32_t>(n, 1);
-  a.count = c.shufC.as<uint32_t>();
-  a.n = n;
-  a.s0 = rng_keyed2(seed, kStreamPartition, epoch);
-  int per_sm = 0;
-  F2V_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, shuffle_kernel, 256, 0));
-  const int blocks = std::max(1, per_sm) * c.num_sms;
-  void* args[] = {&a};
-  F2V_CUDA(cudaLaunchCooperativeKernel((void*)shuffle_kernel, blocks, 256, args, 0, c.stream));
-  F2V_LAUNCHED(c.stream, "shuffle_kernel");
-  ++c.launches;
+  if (n == 0) return;
+  const uint64_t s0 = rng_keyed2(seed, kStreamPartition, epoch);
+  const uint32_t N = n - 1;  // steps m = 1 .. n-1
+  const size_t nn = std::max<uint32_t>(n, 1);
+  c.shufL.ensure(sizeof(uint32_t) * nn * 8);
+  uint32_t* key = c.shufL.as<uint32_t>();
+  uint32_t* val = key + nn;
+  uint32_t* ks = val + nn;
+  uint32_t* vs = ks + nn;
+  uint32_t* succ = vs + nn;
+  uint32_t* first = succ + nn;
+  uint32_t* p0 = first + nn;
+  uint32_t* p1 = p0 + nn;
+  const uint32_t g = (n + 255) / 256;
+  F2V_CUDA(cudaMemsetAsync(first, 0xff, sizeof(uint32_t) * n, c.stream));
+  if (N) {
+    targets_kernel<<<g, 256, 0, c.stream>>>(key, val, n, s0);
+    F2V_LAUNCHED(c.stream, "targets_kernel");
+    int bits = 1;
+    while (bits < 32 && (uint64_t(1) << bits) < n) ++bits;
+    size_t tmp = 0;
+    F2V_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, ks, val, vs, N, 0, bits,
+                                             c.stream));
+    c.shufR.ensure(tmp);
+    F2V_CUDA(cub::DeviceRadixSort::SortPairs(c.shufR.p, tmp, key, ks, val, vs, N, 0, bits,
+                                             c.stream));
+    groups_kernel<<<(N + 255) / 256, 256, 0, c.stream>>>(ks, vs, N, succ, first);
+    F2V_LAUNCHED(c.stream, "groups_kernel");
+  }
+  next_kernel<<<g, 256, 0, c.stream>>>(succ, first, p0, n);
+  F2V_LAUNCHED(c.stream, "next_kernel");
+  // pointer jumping: chains are strictly increasing, so ceil(log2 n) rounds suffice
+  uint32_t* in = p0;
+  uint32_t* out = p1;
+  for (uint64_t span = 1; span < n; span <<= 1) {
+    jump_kernel<<<g, 256, 0, c.stream>>>(in, out, n);
+    F2V_LAUNCHED(c.stream, "jump_kernel");
+    std::swap(in, out);
+  }
+  final_kernel<<<g, 256, 0, c.stream>>>(succ, first, in, perm_out, n, s0);
+  F2V_LAUNCHED(c.stream, "final_kernel");
+  c.launches += 6;
 }
 
 }  // namespace f2v
