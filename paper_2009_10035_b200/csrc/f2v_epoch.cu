@@ -60,35 +60,26 @@ __global__ void state_kernel(const uint32_t* __restrict__ perm, uint32_t* __rest
   wtot[u] = 0;
 }
 
-// One warp per chunk: count the window arcs of every vertex (integer atomics).
-__global__ void window_scan_kernel(const uint64_t* __restrict__ rowptr,
+// One thread per arc: mark the vertices that have a window arc (batch(v) in
+// [batch(u) - W, batch(u))).  src[] is the static arc -> source map.
+__global__ void window_scan_kernel(const uint32_t* __restrict__ src,
                                    const uint32_t* __restrict__ col,
-                                   const uint32_t* __restrict__ chunk_vertex,
-                                   const uint32_t* __restrict__ cbase,
                                    const uint32_t* __restrict__ state, uint32_t* __restrict__ wtot,
-                                   uint64_t chunks, uint32_t C, uint32_t W) {
-  const uint64_t cs = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+                                   uint64_t nnz, uint32_t W) {
+  const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= nnz) return;
+  const uint32_t u = __ldg(src + e), v = __ldg(col + e);
+  const uint32_t j = __ldg(state + u) >> 1, bv = __ldg(state + v) >> 1;
+  if (bv < j && bv + W >= j) wtot[u] = 1;  // benign race: every writer stores 1
+}
+
+// src[e] = the row of arc e (static per graph)
+__global__ void src_kernel(const uint64_t* __restrict__ rowptr, uint32_t* __restrict__ src,
+                           uint32_t n) {
+  const uint32_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (cs >= chunks) return;
-  const uint32_t u = chunk_vertex[cs];
-  const uint32_t j = state[u] >> 1;
-  if (j == 0) return;  // batch 0 has no earlier batches
-  const uint64_t r0 = rowptr[u], r1 = rowptr[u + 1];
-  const uint64_t e0 = r0 + uint64_t(cs - cbase[u]) * C, e1 = umin64(e0 + C, r1);
-  uint32_t cnt = 0;
-  for (uint64_t e = e0 + lane; e < e1; e += 32 * 8) {  // 8 independent gathers in flight
-    uint32_t v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = e + 32 * i < e1 ? __ldg(col + e + 32 * i) : 0u;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t bv = __ldg(state + v[i]) >> 1;
-      cnt += (e + 32 * i < e1 && bv < j && bv + W >= j) ? 1u : 0u;
-    }
-  }
-#pragma unroll
-  for (int m = 16; m; m >>= 1) cnt += __shfl_xor_sync(kFull, cnt, m);
-  if (lane == 0 && cnt) atomicAdd(wtot + u, cnt);
+  if (u >= n) return;
+  for (uint64_t e = rowptr[u] + lane; e < rowptr[u + 1]; e += 32) src[e] = u;
 }
 
 __global__ void needs_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint32_t b,
@@ -178,7 +169,6 @@ void load_tuning(EpochTuning& t) {
 void k_prepare_graph(Ctx& c) {
   const uint32_t C = c.tune.chunk, G = c.tune.lgroup;
   std::vector<uint32_t> cbase(size_t(c.n) + 1), lbase(size_t(c.n) + 1), lpo(c.n ? c.n : 1, 0u);
-  std::vector<uint32_t> cvert;
   uint64_t chunks = 0, lgroups = 0, lslots = 0;
   for (uint32_t u = 0; u < c.n; ++u) {
     const uint64_t deg = c.h_rowptr[u + 1] - c.h_rowptr[u];
@@ -197,9 +187,6 @@ void k_prepare_graph(Ctx& c) {
   }
   cbase[c.n] = uint32_t(chunks);
   lbase[c.n] = uint32_t(lgroups);
-  cvert.resize(std::max<uint64_t>(chunks, 1));
-  for (uint32_t u = 0; u < c.n; ++u)
-    for (uint32_t q = cbase[u]; q < cbase[u + 1]; ++q) cvert[q] = u;
   c.chunks = chunks;
   c.lgroups = lgroups;
   c.lslots = lslots;
@@ -208,7 +195,7 @@ void k_prepare_graph(Ctx& c) {
   c.cbase.ensure(sizeof(uint32_t) * (size_t(c.n) + 1));
   c.lbase.ensure(sizeof(uint32_t) * (size_t(c.n) + 1));
   c.lpo.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
-  c.cvert.ensure(sizeof(uint32_t) * cvert.size());
+  c.src.ensure(sizeof(uint32_t) * std::max<uint64_t>(c.nnz, 1));
   c.ecnt.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
   c.lcnt.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
   c.vflag.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
@@ -216,8 +203,11 @@ void k_prepare_graph(Ctx& c) {
                            cudaMemcpyHostToDevice, c.stream));
   F2V_CUDA(cudaMemcpyAsync(c.lbase.p, lbase.data(), sizeof(uint32_t) * (c.n + 1),
                            cudaMemcpyHostToDevice, c.stream));
-  F2V_CUDA(cudaMemcpyAsync(c.cvert.p, cvert.data(), sizeof(uint32_t) * cvert.size(),
-                           cudaMemcpyHostToDevice, c.stream));
+  if (c.n) {
+    src_kernel<<<uint32_t((uint64_t(c.n) * 32 + 255) / 256), 256, 0, c.stream>>>(
+        c.rowptr.as<uint64_t>(), c.src.as<uint32_t>(), c.n);
+    F2V_LAUNCHED(c.stream, "src_kernel");
+  }
   if (c.n) {
     F2V_CUDA(cudaMemcpyAsync(c.lpo.p, lpo.data(), sizeof(uint32_t) * c.n,
                              cudaMemcpyHostToDevice, c.stream));
@@ -264,10 +254,10 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
       c.negs_all.as<uint32_t>(), c.negwin.as<uint32_t>(), c.state.as<uint32_t>(), nb, s, n, seed,
       epoch, sampler, W);
   F2V_LAUNCHED(c.stream, "negs_kernel");
-  window_scan_kernel<<<uint32_t((c.chunks * 32 + 255) / 256), 256, 0, c.stream>>>(
-      c.rowptr.as<uint64_t>(), c.col.as<uint32_t>(), c.cvert.as<uint32_t>(),
-      c.cbase.as<uint32_t>(), c.state.as<uint32_t>(), c.wtot.as<uint32_t>(), c.chunks,
-      c.tune.chunk, W);
+  if (c.nnz)
+    window_scan_kernel<<<uint32_t((c.nnz + 255) / 256), 256, 0, c.stream>>>(
+        c.src.as<uint32_t>(), c.col.as<uint32_t>(), c.state.as<uint32_t>(),
+        c.wtot.as<uint32_t>(), c.nnz, W);
   F2V_LAUNCHED(c.stream, "window_scan_kernel");
   needs_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
       c.perm.as<uint32_t>(), n, b, c.wtot.as<uint32_t>(), c.negwin.as<uint32_t>(),

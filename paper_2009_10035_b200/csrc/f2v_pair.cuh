@@ -261,9 +261,11 @@ __device__ __forceinline__ void rows_exact(const ForceParams& fp, uint32_t packe
   for (int k = 0; k < K; ++k) uu[k] = zu[k];
   for (int k0 = 0; k0 < cnt; k0 += U) {
     float v[U][K];
+    uint32_t pks[U];
 #pragma unroll
     for (int i = 0; i < U; ++i) {
       const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
+      pks[i] = pk;
       if (k0 + i < cnt) {
         const bool coh = (pk & kNewBit) != 0;
         L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, v[i], coh);
@@ -273,11 +275,9 @@ __device__ __forceinline__ void rows_exact(const ForceParams& fp, uint32_t packe
       }
     }
 #pragma unroll
-    for (int i = 0; i < U; ++i) {  // Znew rows not yet final: poll
-      const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
-      if (k0 + i < cnt && (pk & kNewBit))
-        L::poll(znew + size_t(pk & ~kNewBit) * d, lane, d, v[i]);
-    }
+    for (int i = 0; i < U; ++i)  // Znew rows not yet final: poll
+      if (k0 + i < cnt && (pks[i] & kNewBit))
+        L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, v[i]);
     double w[U][K], red[U], nw[U];
 #pragma unroll
     for (int i = 0; i < U; ++i) {
@@ -427,9 +427,11 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
   const int pi = pair_of_lane(lane);
   for (int k0 = 0; k0 < cnt; k0 += 8) {
     float w[8][K];
+    uint32_t pks[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
+      pks[i] = pk;
       if (k0 + i < cnt) {
         const bool coh = (pk & kNewBit) != 0;
         L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, w[i], coh);
@@ -439,11 +441,9 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
       }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {  // Znew rows not yet final: poll
-      const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
-      if (k0 + i < cnt && (pk & kNewBit))
-        L::poll(znew + size_t(pk & ~kNewBit) * d, lane, d, w[i]);
-    }
+    for (int i = 0; i < 8; ++i)  // Znew rows not yet final: poll
+      if (k0 + i < cnt && (pks[i] & kNewBit))
+        L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, w[i]);
     float part[8], nrm[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {

@@ -12,8 +12,8 @@
 //   W(m) = W(next(m)) with next(m) = the smallest step m'' > m targeting m,
 //   and W(m) = m when there is none.
 // Steps are grouped by target with a stable radix sort of (J_m, m); the W
-// chains (strictly increasing step indices) are resolved by pointer jumping.
-// O(n log n) work, ~log2(n) short passes, no sequential loop.
+// chains (strictly increasing step indices, expected length ~ln n) are
+// followed to their roots.  O(n log n) work, a handful of passes.
 #include <cub/device/device_radix_sort.cuh>
 
 #include <algorithm>
@@ -60,10 +60,17 @@ __global__ void next_kernel(const uint32_t* __restrict__ succ, const uint32_t* _
   ptr[m] = f == kNone ? m : f;
 }
 
-__global__ void jump_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+// W(m): follow next() to the chain's root (chains are short: E[length] ~ ln n)
+__global__ void root_kernel(const uint32_t* __restrict__ ptr, uint32_t* __restrict__ W,
                             uint32_t n) {
   const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m < n) out[m] = in[in[m]];
+  if (m >= n) return;
+  uint32_t x = m, y = ptr[m];
+  while (y != x) {
+    x = y;
+    y = ptr[x];
+  }
+  W[m] = x;
 }
 
 __global__ void final_kernel(const uint32_t* __restrict__ succ, const uint32_t* __restrict__ first,
@@ -116,15 +123,9 @@ void k_device_partition(Ctx& c, uint32_t n, uint64_t seed, uint32_t epoch, uint3
   }
   next_kernel<<<g, 256, 0, c.stream>>>(succ, first, p0, n);
   F2V_LAUNCHED(c.stream, "next_kernel");
-  // pointer jumping: chains are strictly increasing, so ceil(log2 n) rounds suffice
-  uint32_t* in = p0;
-  uint32_t* out = p1;
-  for (uint64_t span = 1; span < n; span <<= 1) {
-    jump_kernel<<<g, 256, 0, c.stream>>>(in, out, n);
-    F2V_LAUNCHED(c.stream, "jump_kernel");
-    std::swap(in, out);
-  }
-  final_kernel<<<g, 256, 0, c.stream>>>(succ, first, in, perm_out, n, s0);
+  root_kernel<<<g, 256, 0, c.stream>>>(p0, p1, n);
+  F2V_LAUNCHED(c.stream, "root_kernel");
+  final_kernel<<<g, 256, 0, c.stream>>>(succ, first, p1, perm_out, n, s0);
   F2V_LAUNCHED(c.stream, "final_kernel");
   c.launches += 6;
 }
