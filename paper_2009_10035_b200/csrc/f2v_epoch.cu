@@ -65,12 +65,12 @@ __global__ void state_kernel(const uint32_t* __restrict__ perm, uint32_t* __rest
 __global__ void window_scan_kernel(const uint32_t* __restrict__ src,
                                    const uint32_t* __restrict__ col,
                                    const uint32_t* __restrict__ state, uint32_t* __restrict__ wtot,
-                                   uint64_t nnz, uint32_t W) {
+                                   uint64_t nnz, uint32_t W, uint32_t Re) {
   const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= nnz) return;
   const uint32_t u = __ldg(src + e), v = __ldg(col + e);
   const uint32_t j = __ldg(state + u) >> 1, bv = __ldg(state + v) >> 1;
-  if (bv < j && bv + W >= j) wtot[u] = 1;  // benign race: every writer stores 1
+  if (bv < j && bv + W >= j) atomicOr(wtot + u, bv + Re >= j ? 3u : 1u);  // bit1: engine-recent
 }
 
 // src[e] = the row of arc e (static per graph)
@@ -85,17 +85,21 @@ __global__ void src_kernel(const uint64_t* __restrict__ rowptr, uint32_t* __rest
 __global__ void needs_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint32_t b,
                              const uint32_t* __restrict__ wtot, const uint32_t* __restrict__ negwin,
                              const uint32_t* __restrict__ lbase, uint32_t* __restrict__ needs,
-                             uint32_t* __restrict__ nL, int nodep) {
+                             uint32_t* __restrict__ nL, uint32_t* __restrict__ nEng, int nodep) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > n) return;
   if (p == n) {
     nL[n] = 0;
+    nEng[n] = 0;
     return;
   }
   const uint32_t u = perm[p];
-  const uint32_t nd = (wtot[u] > 0 || negwin[p / b] != 0) && !nodep ? 1u : 0u;
+  const uint32_t nw = negwin[p / b];
+  uint32_t nd = ((wtot[u] | nw) & 1u) && !nodep ? 1u : 0u;
+  if (nd && ((wtot[u] | nw) & 2u)) nd |= 2u;  // the chain engine finalises it
   needs[u] = nd;
   nL[p] = nd ? lbase[u + 1] - lbase[u] : 0u;
+  nEng[p] = (nd & 2u) ? 1u : 0u;
 }
 
 __global__ void emit_kernel(const uint32_t* __restrict__ P, const uint32_t* __restrict__ cnt,
@@ -107,9 +111,21 @@ __global__ void emit_kernel(const uint32_t* __restrict__ P, const uint32_t* __re
   (void)cnt;
 }
 
+// engine positions (batch-major) and each engine vertex's slot in its batch
+__global__ void engine_emit_kernel(const uint32_t* __restrict__ ecum,
+                                   const uint32_t* __restrict__ nEng,
+                                   const uint32_t* __restrict__ perm, uint32_t* __restrict__ epos,
+                                   uint32_t* __restrict__ eslot, uint32_t n, uint32_t b) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n || !nEng[p]) return;
+  epos[ecum[p]] = p;
+  eslot[perm[p]] = ecum[p] - ecum[uint64_t(p / b) * b];
+}
+
 __global__ void negs_kernel(uint32_t* __restrict__ out, uint32_t* __restrict__ negwin,
                             const uint32_t* __restrict__ state, uint64_t nb, uint32_t s,
-                            uint32_t n, uint64_t seed, uint32_t epoch, int sampler, uint32_t W) {
+                            uint32_t n, uint64_t seed, uint32_t epoch, int sampler, uint32_t W,
+                            uint32_t Re) {
   const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= nb) return;
   uint32_t win = 0;
@@ -118,7 +134,7 @@ __global__ void negs_kernel(uint32_t* __restrict__ out, uint32_t* __restrict__ n
                                                      : splitmix_negative(seed, epoch, j, 0, 1, k, n);
     out[j * s + k] = w;
     const uint32_t bw = state[w] >> 1;
-    if (bw < j && uint64_t(bw) + W >= j) win = 1;
+    if (bw < j && uint64_t(bw) + W >= j) win |= uint64_t(bw) + Re >= j ? 3u : 1u;
   }
   negwin[j] = win;
 }
@@ -163,6 +179,8 @@ void load_tuning(EpochTuning& t) {
   t.recent = env_u32("F2V_RECENT", t.recent);
   t.lwarps = std::min(uint32_t(ep::kWarps - 1), std::max(1u, env_u32("F2V_LWARPS", t.lwarps)));
   if (const char* e = std::getenv("F2V_PRECISION")) t.fast = std::strcmp(e, "exact") != 0;
+  t.erecent = env_u32("F2V_ERECENT", t.erecent);
+  if (t.erecent >= t.window) t.erecent = t.window - 1;
 }
 
 // Static per-graph chunk / L-group layout (depends on chunk and lgroup only).
@@ -245,6 +263,13 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
   c.ploss.ensure(sizeof(double) * std::max<uint32_t>(n, 1));
   c.counters.ensure(64);
   const uint32_t W = c.tune.window;
+  const uint32_t Re = c.tune.erecent;  // 0: no chain engine
+  c.nEng.ensure(sizeof(uint32_t) * (n + 1));
+  c.ecum.ensure(sizeof(uint32_t) * (n + 1));
+  c.epos.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  c.eslot.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  c.rcnt.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  c.lrc.ensure(sizeof(uint32_t) * std::max<uint64_t>(c.lslots, 1));
   state_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(c.perm.as<uint32_t>(),
                                                          c.state.as<uint32_t>(), n, b,
                                                          c.cbase.as<uint32_t>(),
@@ -252,16 +277,16 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
   F2V_LAUNCHED(c.stream, "state_kernel");
   negs_kernel<<<(nb + 255) / 256, 256, 0, c.stream>>>(
       c.negs_all.as<uint32_t>(), c.negwin.as<uint32_t>(), c.state.as<uint32_t>(), nb, s, n, seed,
-      epoch, sampler, W);
+      epoch, sampler, W, Re);
   F2V_LAUNCHED(c.stream, "negs_kernel");
   if (c.nnz)
     window_scan_kernel<<<uint32_t((c.nnz + 255) / 256), 256, 0, c.stream>>>(
         c.src.as<uint32_t>(), c.col.as<uint32_t>(), c.state.as<uint32_t>(),
-        c.wtot.as<uint32_t>(), c.nnz, W);
+        c.wtot.as<uint32_t>(), c.nnz, W, Re);
   F2V_LAUNCHED(c.stream, "window_scan_kernel");
   needs_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
       c.perm.as<uint32_t>(), n, b, c.wtot.as<uint32_t>(), c.negwin.as<uint32_t>(),
-      c.lbase.as<uint32_t>(), c.needs.as<uint32_t>(), c.nL.as<uint32_t>(),
+      c.lbase.as<uint32_t>(), c.needs.as<uint32_t>(), c.nL.as<uint32_t>(), c.nEng.as<uint32_t>(),
       std::getenv("F2V_DEBUG_NODEP") ? 1 : 0);
   F2V_LAUNCHED(c.stream, "needs_kernel");
   size_t tmp = 0;
@@ -278,6 +303,14 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
   emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.LP.as<uint32_t>(), c.nL.as<uint32_t>(),
                                                      c.litems.as<uint2>(), n);
   F2V_LAUNCHED(c.stream, "emit_kernel");
+  if (Re) {
+    F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.nEng.as<uint32_t>(),
+                                           c.ecum.as<uint32_t>(), n + 1, c.stream));
+    engine_emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(
+        c.ecum.as<uint32_t>(), c.nEng.as<uint32_t>(), c.perm.as<uint32_t>(), c.epos.as<uint32_t>(),
+        c.eslot.as<uint32_t>(), n, b);
+    F2V_LAUNCHED(c.stream, "engine_emit_kernel");
+  }
   // number of L items (device value, read back asynchronously with the run)
   F2V_CUDA(cudaMemcpyAsync(c.counters.as<uint32_t>() + 8, c.LP.as<uint32_t>() + n,
                            sizeof(uint32_t), cudaMemcpyDeviceToDevice, c.stream));
@@ -338,6 +371,16 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.W = c.tune.window;
   a.R = c.tune.recent;
   a.lwarps = c.tune.lwarps;
+  a.Re = c.tune.erecent;
+  a.rcnt = c.rcnt.as<uint32_t>();
+  a.lrc = c.lrc.as<uint32_t>();
+  a.epos = c.epos.as<uint32_t>();
+  a.ecum = c.ecum.as<uint32_t>();
+  a.eslot = c.eslot.as<uint32_t>();
+  a.maxe = a.Re ? uint32_t(std::min<size_t>(64, (200u * 1024u) / (size_t(a.Re + 1) * c.d * 4)))
+                : 0u;
+  if (a.Re && a.maxe == 0) a.Re = 0;  // rows too wide for a ring: no engine
+  if (a.Re && (c.n >= kIdMask)) a.Re = 0;
   a.eta = eta;
   a.fp = fp;
   a.nodep = std::getenv("F2V_DEBUG_NODEP") ? 1 : 0;

@@ -57,6 +57,13 @@ struct EpochArgs {
   unsigned long long* bad;
   uint32_t n, d, b, s;
   uint32_t C, G, W, R, lwarps;
+  uint32_t Re;              // chain engine: arcs of age <= Re are the engine's (0 = off)
+  uint32_t* rcnt;           // per vertex: recent (age <= Re) arc count, one-L-item vertices
+  uint32_t* lrc;            // per L partial slot: recent arc count (hub vertices)
+  const uint32_t* epos;     // engine: list of engine positions, batch-major
+  const uint32_t* ecum;     // engine: exclusive count of engine positions (n + 1)
+  const uint32_t* eslot;    // engine: per vertex index within its batch's engine list
+  uint32_t maxe;            // engine: ring rows per batch
   float eta;
   ForceParams fp;
   uint64_t nnz, chunks, lslots;  // bounds, used by F2V_DEVICE_CHECKS builds
@@ -151,7 +158,7 @@ __device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, int
 template <int K, bool VEC, bool MON>
 __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_t u, int lane,
                                          const float (&zu)[K], const double (&acc)[K],
-                                         double lsum) {
+                                         double lsum, float* ring_row = nullptr) {
   using L = Lay<K, VEC>;
   bool bad = false;
   float nz[K];
@@ -162,6 +169,7 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_
     nz[k] = __fsub_rn(zu[k], __fmul_rn(a.eta, g));
     if (nz[k] != nz[k]) nz[k] = __int_as_float(0x7fffffff);  // never the sentinel NaN
   }
+  if (ring_row) L::store_smem(ring_row, lane, a.d, nz);    // the chain engine's own copy
   L::store(a.znew + size_t(u) * a.d, lane, a.d, nz);  // publishes the row (sentinel-free)
   const bool any_bad = __any_sync(kFull, bad);
   if (MON) {
@@ -307,8 +315,9 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, u
                                                uint32_t c0, uint32_t c1, int lane,
                                                uint32_t* qbuf, uint32_t* rbuf, int& nr,
                                                const float (&zu)[K], double (&acc)[K],
-                                               double& lsum) {
+                                               double& lsum, bool defer = false) {
   const uint64_t r0 = a.rowptr[u];
+  const uint64_t obase = r0 + uint64_t(c0) * a.C;  // engine mode: recent ids written here
   const uint32_t cb = a.cbase[u];
   RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0};
   for (uint32_t cc = c0; cc < c1; cc += 32) {
@@ -343,12 +352,17 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, u
         DCHECK(v < a.n, "L wl v=%u", v);
         st = ld_relaxed(a.state + v);
         const uint32_t age = j - (st >> 1);
-        old = age > a.R;
+        old = age > (defer ? a.Re : a.R);
         recent = !old;
       }
       q.push(a, lane, old, v | kNewBit, zu, acc, lsum);
-      // park the recent ones (processed in place if the parking lot is full)
       const uint32_t rm = __ballot_sync(kFull, recent);
+      if (defer) {  // engine mode: the recent arcs are the chain engine's (compacted ids)
+        if (recent) a.wl[obase + nr + __popc(rm & lanemask_lt(lane))] = v;
+        nr += __popc(rm);
+        continue;
+      }
+      // park the recent ones (processed in place if the parking lot is full)
       if (nr + __popc(rm) > kRq) {
         q.flush(a, lane, zu, acc, lsum);
         recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
@@ -388,10 +402,29 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   }
   if (lt && lane == 0) lt[1] = globaltimer();
   const uint32_t c0 = cl * a.G, c1 = umin32(nch, c0 + a.G);
-  if (nchL == 1) {  // E total + old window arcs + negatives + recent arcs
+  const uint32_t nflag = a.needs[u];
+  const bool eng = (nflag & 2u) != 0;          // the chain engine finalises u
+  const bool negs_here = !(eng && (a.negwin[j] & 2u));  // recent negatives: the engine's
+  if (nchL == 1) {
     L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __ldcg(a.eloss + cb);
     int nr = 0;
+    if (eng) {  // E total + old window arcs + negatives -> pre-final partial P(u)
+      window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
+                                              lsum, true);
+      if (negs_here) do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+      L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
+      const double ls = MON ? warp_sum_d(lsum) : 0.0;
+      if (lane == 0) {
+        if (MON) __stcg(a.eloss + cb, ls);
+        __stcg(a.rcnt + u, uint32_t(nr));
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_relaxed(a.vflag + u, 2u);
+      return;
+    }
+    // E total + old window arcs + negatives + recent arcs
     window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
     do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
     if (lt && lane == 0) lt[2] = globaltimer();
@@ -402,15 +435,19 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     return;
   }
   int nr = 0;
-  window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
-  recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
+  window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum,
+                                          eng);
+  if (!eng) recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
   const uint32_t slot = a.lpo[u] + cl;
   DCHECK(slot < a.lslots, "L slot=%u lslots=%llu cl=%u nchL=%u", slot,
          (unsigned long long)a.lslots, cl, nchL);
   L::store_acc(a.lpart + size_t(slot) * a.d, lane, a.d, acc);
   {
     const double ls = MON ? warp_sum_d(lsum) : 0.0;
-    if (MON && lane == 0) __stcg(a.lloss + slot, ls);
+    if (lane == 0) {
+      if (MON) __stcg(a.lloss + slot, ls);
+      if (eng) __stcg(a.lrc + slot, uint32_t(nr));
+    }
   }
   __threadfence();
   __syncwarp();
@@ -426,12 +463,18 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     L::add_acc(a.lpart + size_t(lp + qq) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __dadd_rn(lsum, __ldcg(a.lloss + lp + qq));
   }
-  do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
-  finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
-  if (lane == 0) {
-    a.lcnt[u] = 0;
-    a.vflag[u] = 0;
+  if (negs_here) do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+  if (lane == 0) a.lcnt[u] = 0;
+  if (eng) {  // pre-final partial for the engine
+    L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
+    if (MON && lane == 0) __stcg(a.eloss + cb, lsum);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_relaxed(a.vflag + u, 2u);
+    return;
   }
+  finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
+  if (lane == 0) a.vflag[u] = 0;
 }
 
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
@@ -460,6 +503,81 @@ __global__ void __launch_bounds__(kWarps * 32, 2) epoch_kernel(EpochArgs a) {
   }
 }
 
+// The chain engine: ONE CTA that walks the batches
+// of the epoch in order and finalises the vertices that have arcs to the last
+// Re batches (or a batch whose negatives are that recent).  Their L items hand
+// it a pre-final partial P(u) (E total + older window arcs + negatives) and the
+// compacted list of recent arcs; the engine adds those pairs and finalises.
+// Rows it finalised in the last Re batches stay in a shared-memory ring, so a
+// batch-to-batch dependency costs a __syncthreads and a shared load instead of
+// global-memory round trips.  Batch j's ring rows are reused at batch j+Re+1.
+constexpr int kEngineWarps = 16;
+
+template <int KIND, int K, bool VEC, bool MON, bool FAST>
+__global__ void __launch_bounds__(kEngineWarps * 32, 1) engine_kernel(EpochArgs a) {
+  extern __shared__ float4 ring4[];
+  float* ring = reinterpret_cast<float*>(ring4);
+  using L = Lay<K, VEC>;
+  const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
+  const uint32_t nb = (a.n + a.b - 1) / a.b;
+  const uint32_t RS = a.Re + 1;
+  for (uint32_t j = 0; j < nb; ++j) {
+    const uint32_t s0 = __ldg(a.ecum + umin64(uint64_t(j) * a.b, a.n));
+    const uint32_t s1 = __ldg(a.ecum + umin64(uint64_t(j + 1) * a.b, a.n));
+    for (uint32_t i = s0 + w; i < s1; i += kEngineWarps) {
+      const uint32_t p = __ldg(a.epos + i);
+      const uint32_t u = a.perm[p];
+      const uint32_t cb = a.cbase[u];
+      const uint32_t nchL = a.lbase[u + 1] - a.lbase[u];
+      const uint64_t r0 = a.rowptr[u];
+      float zu[K];
+      L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
+      uint32_t f = ld_relaxed(a.vflag + u);
+      while (f != 2u) {  // the L items' pre-final partial
+        __nanosleep(20);
+        f = ld_relaxed(a.vflag + u);
+      }
+      double acc[K];
+      L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
+      double lsum = (MON && lane == 0) ? __ldcg(a.eloss + cb) : 0.0;
+      for (uint32_t q = 0; q < nchL; ++q) {
+        const uint32_t cnt = nchL == 1 ? __ldcg(a.rcnt + u) : __ldcg(a.lrc + a.lpo[u] + q);
+        const uint64_t base = r0 + uint64_t(q) * a.G * a.C;
+        for (uint32_t k0 = 0; k0 < cnt; k0 += 32) {
+          const int c = int(umin32(32, cnt - k0));
+          uint32_t pk = 0;
+          if (lane < c) {
+            const uint32_t v = __ldcg(a.wl + base + k0 + lane);
+            const uint32_t bv = __ldg(a.state + v) >> 1;
+            const uint32_t es = __ldg(a.eslot + v);
+            const bool in_ring = (__ldg(a.needs + v) & 2u) && es < a.maxe;
+            pk = in_ring ? (kRingBit | ((bv % RS) * a.maxe + es)) : (v | kNewBit);
+          }
+          Rows<KIND, K, VEC, MON, FAST>::template run<true, true>(a.fp, pk, c, lane, a.d, a.zold,
+                                                                  a.znew, zu, acc, lsum, ring);
+        }
+      }
+      if (a.negwin[j] & 2u) do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+      const uint32_t es = i - s0;
+      float* rrow = es < a.maxe ? ring + (size_t(j % RS) * a.maxe + es) * a.d : nullptr;
+      finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum, rrow);
+      if (lane == 0) a.vflag[u] = 0;
+    }
+    __syncthreads();  // batch j's ring rows are visible to batch j+1
+  }
+}
+
+template <int KIND, int K, bool VEC, bool MON, bool FAST>
+void launch_engine(Ctx& c, const EpochArgs& a) {
+  auto kern = engine_kernel<KIND, K, VEC, MON, FAST>;
+  const size_t smem = size_t(a.Re + 1) * a.maxe * a.d * sizeof(float);
+  F2V_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  kern<<<1, kEngineWarps * 32, smem, c.stream2>>>(a);
+  F2V_LAUNCHED(c.stream2, "engine_kernel");
+  ++c.launches;
+}
+
 // Launch one epoch kernel instantiation as a persistent grid.
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
 void launch_one(Ctx& c, const EpochArgs& a) {
@@ -468,12 +586,26 @@ void launch_one(Ctx& c, const EpochArgs& a) {
   F2V_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0));
   if (per_sm < 1) per_sm = 1;
   uint32_t blocks = uint32_t(per_sm) * uint32_t(c.num_sms);
+  if (a.Re) {
+    // the engine runs concurrently on stream2 (after the prep); leave it room
+    // on any SM (its 16 warps and ring fit beside one epoch CTA) so the two
+    // are co-resident whichever starts first
+    F2V_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    F2V_CUDA(cudaEventRecord(c.ev_prep, c.stream));
+    F2V_CUDA(cudaStreamWaitEvent(c.stream2, c.ev_prep, 0));
+    launch_engine<KIND, K, VEC, MON, FAST>(c, a);
+    blocks = blocks > 2 ? blocks - 2 : 1;
+  }
   const uint64_t ew = kWarps - a.lwarps;
   const uint32_t need = uint32_t(std::max<uint64_t>((a.n_eitems + ew - 1) / ew, 1));
-  blocks = std::max(1u, std::min(blocks, need));
+  blocks = std::max(1u, std::min(blocks, need + (a.Re ? 1u : 0u)));
   kern<<<blocks, kWarps * 32, 0, c.stream>>>(a);
   F2V_LAUNCHED(c.stream, "kern");
   ++c.launches;
+  if (a.Re) {
+    F2V_CUDA(cudaEventRecord(c.ev_engine, c.stream2));
+    F2V_CUDA(cudaStreamWaitEvent(c.stream, c.ev_engine, 0));
+  }
 }
 
 template <int KIND, int K, bool VEC, bool FAST>

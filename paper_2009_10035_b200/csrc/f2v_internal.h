@@ -50,6 +50,7 @@ struct EpochTuning {
   uint32_t recent = 2;   // F2V_RECENT: window arcs this recent are taken last
   uint32_t lwarps = 2;   // F2V_LWARPS: L-role warps per 8-warp CTA
   uint32_t fast = 1;     // F2V_PRECISION=exact|fast: pair math precision (config)
+  uint32_t erecent = 8;  // F2V_ERECENT: chain engine takes arcs of age <= this (0 = off)
 };
 void load_tuning(EpochTuning& t);
 
@@ -84,6 +85,9 @@ struct Ctx {
   DeviceBuf perm, state, negs_all, negwin, items, litems, nE, nL, EP, LP, wtot, needs, scan_tmp,
       epart, eloss, wcnt, wl, lpart, lloss, ploss, counters;
   uint32_t last_litems = 0;
+  DeviceBuf nEng, ecum, epos, eslot, rcnt, lrc;   // chain engine lists
+  cudaStream_t stream2 = nullptr;                 // the chain engine runs here
+  cudaEvent_t ev_prep = nullptr, ev_engine = nullptr;
   DeviceBuf trace;  // DEBUG: per-position finalise timestamps (F2V_TRACE)
   DeviceBuf shufR, shufL;  // device Fisher-Yates (f2v_perm.cu)
 
