@@ -268,7 +268,7 @@ void f2v_destroy(f2v_ctx* h) {
         &c.state, &c.negs_all, &c.negwin, &c.items, &c.litems, &c.nE, &c.nL, &c.EP, &c.LP,
         &c.wtot, &c.needs, &c.scan_tmp, &c.epart, &c.eloss, &c.wcnt, &c.wl, &c.lpart, &c.lloss,
         &c.ploss, &c.counters, &c.trace, &c.shufR, &c.shufL, &c.nEng, &c.ecum, &c.epos,
-        &c.eslot, &c.rcnt, &c.lrc})
+        &c.eslot, &c.eidx, &c.rcnt})
     b->release();
   for (cudaEvent_t e : c.ev_kernel) cudaEventDestroy(e);
   if (c.ev_begin) cudaEventDestroy(c.ev_begin);

@@ -96,7 +96,7 @@ __global__ void needs_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint
   const uint32_t u = perm[p];
   const uint32_t nw = negwin[p / b];
   uint32_t nd = ((wtot[u] | nw) & 1u) && !nodep ? 1u : 0u;
-  if (nd && ((wtot[u] | nw) & 2u)) nd |= 2u;  // the chain engine finalises it
+  if (nd && (wtot[u] & 2u) && lbase[u + 1] - lbase[u] == 1) nd |= 2u;  // the chain engine's
   needs[u] = nd;
   nL[p] = nd ? lbase[u + 1] - lbase[u] : 0u;
   nEng[p] = (nd & 2u) ? 1u : 0u;
@@ -114,12 +114,16 @@ __global__ void emit_kernel(const uint32_t* __restrict__ P, const uint32_t* __re
 // engine positions (batch-major) and each engine vertex's slot in its batch
 __global__ void engine_emit_kernel(const uint32_t* __restrict__ ecum,
                                    const uint32_t* __restrict__ nEng,
-                                   const uint32_t* __restrict__ perm, uint32_t* __restrict__ epos,
-                                   uint32_t* __restrict__ eslot, uint32_t n, uint32_t b) {
+                                   const uint32_t* __restrict__ perm,
+                                   const uint32_t* __restrict__ cbase, uint4* __restrict__ erec,
+                                   uint32_t* __restrict__ eslot, uint32_t* __restrict__ eidx,
+                                   uint32_t n, uint32_t b) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n || !nEng[p]) return;
-  epos[ecum[p]] = p;
-  eslot[perm[p]] = ecum[p] - ecum[uint64_t(p / b) * b];
+  const uint32_t u = perm[p], i = ecum[p];
+  erec[i] = make_uint4(u, cbase[u], p, 0u);
+  eslot[u] = i - ecum[uint64_t(p / b) * b];
+  eidx[u] = i;
 }
 
 __global__ void negs_kernel(uint32_t* __restrict__ out, uint32_t* __restrict__ negwin,
@@ -266,10 +270,10 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
   const uint32_t Re = c.tune.erecent;  // 0: no chain engine
   c.nEng.ensure(sizeof(uint32_t) * (n + 1));
   c.ecum.ensure(sizeof(uint32_t) * (n + 1));
-  c.epos.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  c.epos.ensure(sizeof(uint4) * std::max<uint32_t>(n, 1));
   c.eslot.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
-  c.rcnt.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
-  c.lrc.ensure(sizeof(uint32_t) * std::max<uint64_t>(c.lslots, 1));
+  c.eidx.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  c.rcnt.ensure(sizeof(uint32_t) * ep::kRefStride * std::max<uint32_t>(n, 1));
   state_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(c.perm.as<uint32_t>(),
                                                          c.state.as<uint32_t>(), n, b,
                                                          c.cbase.as<uint32_t>(),
@@ -307,8 +311,9 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
     F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.nEng.as<uint32_t>(),
                                            c.ecum.as<uint32_t>(), n + 1, c.stream));
     engine_emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(
-        c.ecum.as<uint32_t>(), c.nEng.as<uint32_t>(), c.perm.as<uint32_t>(), c.epos.as<uint32_t>(),
-        c.eslot.as<uint32_t>(), n, b);
+        c.ecum.as<uint32_t>(), c.nEng.as<uint32_t>(), c.perm.as<uint32_t>(),
+        c.cbase.as<uint32_t>(), c.epos.as<uint4>(), c.eslot.as<uint32_t>(),
+        c.eidx.as<uint32_t>(), n, b);
     F2V_LAUNCHED(c.stream, "engine_emit_kernel");
   }
   // number of L items (device value, read back asynchronously with the run)
@@ -372,15 +377,20 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.R = c.tune.recent;
   a.lwarps = c.tune.lwarps;
   a.Re = c.tune.erecent;
-  a.rcnt = c.rcnt.as<uint32_t>();
-  a.lrc = c.lrc.as<uint32_t>();
-  a.epos = c.epos.as<uint32_t>();
+  a.rl = c.rcnt.as<uint32_t>();
+  a.erec = c.epos.as<uint4>();
   a.ecum = c.ecum.as<uint32_t>();
   a.eslot = c.eslot.as<uint32_t>();
-  a.maxe = a.Re ? uint32_t(std::min<size_t>(64, (200u * 1024u) / (size_t(a.Re + 1) * c.d * 4)))
-                : 0u;
-  if (a.Re && a.maxe == 0) a.Re = 0;  // rows too wide for a ring: no engine
-  if (a.Re && (c.n >= kIdMask)) a.Re = 0;
+  a.eidx = c.eidx.as<uint32_t>();
+  {  // ring rows per batch: what is left of ~210 KB after the engine's staging area
+    const size_t stage = size_t(ep::kEngineWarps) * ep::kStage *
+                         ((size_t(c.d) * 12 + ep::kRefStride * 4 + 15) / 16 * 16);
+    const size_t budget = 210u * 1024u > stage ? 210u * 1024u - stage : 0;
+    a.maxe = a.Re ? uint32_t(std::min<size_t>(64, budget / (size_t(a.Re + 1) * c.d * 4))) : 0u;
+  }
+  // no engine for rows too wide for a ring, huge n, or the masked row layouts
+  if (a.Re && (a.maxe < 4 || c.n >= kIdMask || (c.d != 64 && c.d != 128 && c.d != 256)))
+    a.Re = 0;
   a.eta = eta;
   a.fp = fp;
   a.nodep = std::getenv("F2V_DEBUG_NODEP") ? 1 : 0;

@@ -25,6 +25,8 @@ using namespace dev;
 constexpr int kWarps = 8;       // warps per CTA
 constexpr int kQ = 64;          // per-warp compaction queue (entries)
 constexpr int kRq = 64;         // per-warp parking lot for the most recent window arcs
+constexpr int kRefs = 32;       // engine: ring refs per vertex (+1 count word); more go global
+constexpr int kRefStride = 36;  // words per vertex ref area (16-byte multiple for cp.async)
 
 struct EpochArgs {
   const uint64_t* rowptr;
@@ -57,12 +59,12 @@ struct EpochArgs {
   unsigned long long* bad;
   uint32_t n, d, b, s;
   uint32_t C, G, W, R, lwarps;
-  uint32_t Re;              // chain engine: arcs of age <= Re are the engine's (0 = off)
-  uint32_t* rcnt;           // per vertex: recent (age <= Re) arc count, one-L-item vertices
-  uint32_t* lrc;            // per L partial slot: recent arc count (hub vertices)
-  const uint32_t* epos;     // engine: list of engine positions, batch-major
+  uint32_t Re;              // chain engine: arcs of age <= Re to ring rows are its (0 = off)
+  uint32_t* rl;             // engine: per engine vertex [count, ring refs...] (kRefs words)
+  const uint4* erec;        // engine: per engine index {vertex, cbase, position, 0}
   const uint32_t* ecum;     // engine: exclusive count of engine positions (n + 1)
   const uint32_t* eslot;    // engine: per vertex index within its batch's engine list
+  const uint32_t* eidx;     // engine: per vertex global engine index
   uint32_t maxe;            // engine: ring rows per batch
   float eta;
   ForceParams fp;
@@ -352,16 +354,27 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, u
         DCHECK(v < a.n, "L wl v=%u", v);
         st = ld_relaxed(a.state + v);
         const uint32_t age = j - (st >> 1);
-        old = age > (defer ? a.Re : a.R);
-        recent = !old;
+        if (defer) {  // engine mode: arcs to rows in the engine's ring are the engine's
+          recent = age <= a.Re && (__ldg(a.needs + v) & 2u) && __ldg(a.eslot + v) < a.maxe;
+          old = !recent;
+        } else {
+          old = age > a.R;
+          recent = !old;
+        }
       }
-      q.push(a, lane, old, v | kNewBit, zu, acc, lsum);
       const uint32_t rm = __ballot_sync(kFull, recent);
-      if (defer) {  // engine mode: the recent arcs are the chain engine's (compacted ids)
-        if (recent) a.wl[obase + nr + __popc(rm & lanemask_lt(lane))] = v;
-        nr += __popc(rm);
+      if (defer) {
+        // ring refs beyond kRefs are taken here, from the global copy of the row
+        const int rank = nr + __popc(rm & lanemask_lt(lane));
+        const bool keep = recent && rank < kRefs;
+        if (keep)
+          a.rl[size_t(a.eidx[u]) * kRefStride + 1 + rank] =
+              kRingBit | (((st >> 1) % (a.Re + 1)) * a.maxe + __ldg(a.eslot + v));
+        q.push(a, lane, old || (recent && !keep), v | kNewBit, zu, acc, lsum);
+        nr = min(kRefs, nr + __popc(rm));
         continue;
       }
+      q.push(a, lane, old, v | kNewBit, zu, acc, lsum);
       // park the recent ones (processed in place if the parking lot is full)
       if (nr + __popc(rm) > kRq) {
         q.flush(a, lane, zu, acc, lsum);
@@ -403,21 +416,20 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   if (lt && lane == 0) lt[1] = globaltimer();
   const uint32_t c0 = cl * a.G, c1 = umin32(nch, c0 + a.G);
   const uint32_t nflag = a.needs[u];
-  const bool eng = (nflag & 2u) != 0;          // the chain engine finalises u
-  const bool negs_here = !(eng && (a.negwin[j] & 2u));  // recent negatives: the engine's
+  const bool eng = (nflag & 2u) != 0;  // the chain engine finalises u (one-L-item vertices)
   if (nchL == 1) {
     L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __ldcg(a.eloss + cb);
     int nr = 0;
-    if (eng) {  // E total + old window arcs + negatives -> pre-final partial P(u)
+    if (eng) {  // E total + window arcs except ring refs + negatives -> pre-final P(u)
       window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
                                               lsum, true);
-      if (negs_here) do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+      do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
       L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
       const double ls = MON ? warp_sum_d(lsum) : 0.0;
       if (lane == 0) {
         if (MON) __stcg(a.eloss + cb, ls);
-        __stcg(a.rcnt + u, uint32_t(nr));
+        __stcg(a.rl + size_t(a.eidx[u]) * kRefStride, uint32_t(nr));
       }
       __threadfence();
       __syncwarp();
@@ -435,19 +447,15 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     return;
   }
   int nr = 0;
-  window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum,
-                                          eng);
-  if (!eng) recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
+  window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
+  recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
   const uint32_t slot = a.lpo[u] + cl;
   DCHECK(slot < a.lslots, "L slot=%u lslots=%llu cl=%u nchL=%u", slot,
          (unsigned long long)a.lslots, cl, nchL);
   L::store_acc(a.lpart + size_t(slot) * a.d, lane, a.d, acc);
   {
     const double ls = MON ? warp_sum_d(lsum) : 0.0;
-    if (lane == 0) {
-      if (MON) __stcg(a.lloss + slot, ls);
-      if (eng) __stcg(a.lrc + slot, uint32_t(nr));
-    }
+    if (MON && lane == 0) __stcg(a.lloss + slot, ls);
   }
   __threadfence();
   __syncwarp();
@@ -463,16 +471,8 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     L::add_acc(a.lpart + size_t(lp + qq) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __dadd_rn(lsum, __ldcg(a.lloss + lp + qq));
   }
-  if (negs_here) do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+  do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
   if (lane == 0) a.lcnt[u] = 0;
-  if (eng) {  // pre-final partial for the engine
-    L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
-    if (MON && lane == 0) __stcg(a.eloss + cb, lsum);
-    __threadfence();
-    __syncwarp();
-    if (lane == 0) st_relaxed(a.vflag + u, 2u);
-    return;
-  }
   finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
   if (lane == 0) a.vflag[u] = 0;
 }
@@ -504,78 +504,142 @@ __global__ void __launch_bounds__(kWarps * 32, 2) epoch_kernel(EpochArgs a) {
 }
 
 // The chain engine: ONE CTA that walks the batches
-// of the epoch in order and finalises the vertices that have arcs to the last
-// Re batches (or a batch whose negatives are that recent).  Their L items hand
-// it a pre-final partial P(u) (E total + older window arcs + negatives) and the
-// compacted list of recent arcs; the engine adds those pairs and finalises.
-// Rows it finalised in the last Re batches stay in a shared-memory ring, so a
-// batch-to-batch dependency costs a __syncthreads and a shared load instead of
-// global-memory round trips.  Batch j's ring rows are reused at batch j+Re+1.
+// of the epoch in order and finalises the "engine vertices" (one-L-item
+// vertices with arcs to the last Re batches).  Their L items hand it a
+// pre-final partial P(u) (E total + every window arc except those into the
+// engine's ring + the negatives) and the ring references; rows it finalised in
+// the last Re batches stay in a shared-memory ring, so a batch-to-batch
+// dependency costs a __syncthreads and a shared load instead of global-memory
+// round trips.  P(u) and z_u of the next batch are staged into shared memory
+// with cp.async while the current batch computes.  Batch j's ring rows are
+// reused at batch j+Re+1.
 constexpr int kEngineWarps = 16;
+constexpr int kStage = 3;  // staged vertices per warp per batch
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = uint32_t(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
 
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
-__global__ void __launch_bounds__(kEngineWarps * 32, 1) engine_kernel(EpochArgs a) {
-  extern __shared__ float4 ring4[];
-  float* ring = reinterpret_cast<float*>(ring4);
+__global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs a) {
+  extern __shared__ float4 smem4[];
   using L = Lay<K, VEC>;
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const uint32_t nb = (a.n + a.b - 1) / a.b;
+  const uint32_t d = a.d;
   const uint32_t RS = a.Re + 1;
-  for (uint32_t j = 0; j < nb; ++j) {
-    const uint32_t s0 = __ldg(a.ecum + umin64(uint64_t(j) * a.b, a.n));
-    const uint32_t s1 = __ldg(a.ecum + umin64(uint64_t(j + 1) * a.b, a.n));
-    for (uint32_t i = s0 + w; i < s1; i += kEngineWarps) {
-      const uint32_t p = __ldg(a.epos + i);
-      const uint32_t u = a.perm[p];
-      const uint32_t cb = a.cbase[u];
-      const uint32_t nchL = a.lbase[u + 1] - a.lbase[u];
-      const uint64_t r0 = a.rowptr[u];
-      float zu[K];
-      L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
-      uint32_t f = ld_relaxed(a.vflag + u);
-      while (f != 2u) {  // the L items' pre-final partial
-        __nanosleep(20);
-        f = ld_relaxed(a.vflag + u);
-      }
-      double acc[K];
-      L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
-      double lsum = (MON && lane == 0) ? __ldcg(a.eloss + cb) : 0.0;
-      for (uint32_t q = 0; q < nchL; ++q) {
-        const uint32_t cnt = nchL == 1 ? __ldcg(a.rcnt + u) : __ldcg(a.lrc + a.lpo[u] + q);
-        const uint64_t base = r0 + uint64_t(q) * a.G * a.C;
-        for (uint32_t k0 = 0; k0 < cnt; k0 += 32) {
-          const int c = int(umin32(32, cnt - k0));
-          uint32_t pk = 0;
-          if (lane < c) {
-            const uint32_t v = __ldcg(a.wl + base + k0 + lane);
-            const uint32_t bv = __ldg(a.state + v) >> 1;
-            const uint32_t es = __ldg(a.eslot + v);
-            const bool in_ring = (__ldg(a.needs + v) & 2u) && es < a.maxe;
-            pk = in_ring ? (kRingBit | ((bv % RS) * a.maxe + es)) : (v | kNewBit);
-          }
-          Rows<KIND, K, VEC, MON, FAST>::template run<true, true>(a.fp, pk, c, lane, a.d, a.zold,
-                                                                  a.znew, zu, acc, lsum, ring);
+  float* ring = reinterpret_cast<float*>(smem4);
+  // staging: per warp kStage slots of [P (d doubles) | z_u (d floats) | refs (kRefStride words)]
+  const size_t slot_words = (size_t(d) * 12 + kRefStride * 4 + 15) / 16 * 4;
+  uint32_t* stage = reinterpret_cast<uint32_t*>(ring + size_t(RS) * a.maxe * d) +
+                    size_t(w) * kStage * slot_words;
+  __shared__ uint32_t staged[kEngineWarps][kStage];
+  const uint32_t nb = (a.n + a.b - 1) / a.b;
+
+  auto range = [&](uint32_t j, uint32_t& s0, uint32_t& s1) {
+    s0 = __ldg(a.ecum + umin64(uint64_t(j) * a.b, a.n));
+    s1 = __ldg(a.ecum + umin64(uint64_t(j + 1) * a.b, a.n));
+  };
+  // stage P, z_u and the refs of this warp's first kStage vertices of batch j
+  auto prefetch = [&](uint32_t j) {
+    uint32_t s0, s1;
+    range(j, s0, s1);
+    for (int k = 0; k < kStage; ++k) {
+      const uint32_t i = s0 + w + uint32_t(k) * kEngineWarps;
+      uint32_t ok = 0;
+      if (i < s1) {
+        const uint4 rec = __ldg(a.erec + i);
+        ok = ld_relaxed(a.vflag + rec.x) == 2u;
+        if (ok) {
+          uint32_t* sl = stage + size_t(k) * slot_words;
+          const char* P = reinterpret_cast<const char*>(a.epart + size_t(rec.y) * d);
+          const char* Z = reinterpret_cast<const char*>(a.zold + size_t(rec.x) * d);
+          const char* R = reinterpret_cast<const char*>(a.rl + size_t(i) * kRefStride);
+          char* dst = reinterpret_cast<char*>(sl);
+          for (uint32_t off = lane * 16; off < d * 8; off += 512) cp_async16(dst + off, P + off);
+          for (uint32_t off = lane * 16; off < d * 4; off += 512)
+            cp_async16(dst + d * 8 + off, Z + off);
+          if (lane * 16 < kRefStride * 4) cp_async16(dst + d * 12 + lane * 16, R + lane * 16);
         }
       }
-      if (a.negwin[j] & 2u) do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+      if (lane == 0) staged[w][k] = ok;
+    }
+    cp_async_commit();
+  };
+
+  prefetch(0);
+  for (uint32_t j = 0; j < nb; ++j) {
+    uint32_t s0, s1;
+    range(j, s0, s1);
+    cp_async_wait_all();
+    __syncwarp();
+    int k = 0;
+    for (uint32_t i = s0 + w; i < s1; i += kEngineWarps, ++k) {
+      const uint4 rec = __ldg(a.erec + i);
+      const uint32_t u = rec.x, cb = rec.y, p = rec.z;
+      float zu[K];
+      double acc[K];
+      uint32_t nrefs, myref = 0;
+      const bool st = k < kStage && staged[w][k];
+      if (st) {
+        const uint32_t* sl = stage + size_t(k) * slot_words;
+        const double* sP = reinterpret_cast<const double*>(sl);
+        const float* sZ = reinterpret_cast<const float*>(reinterpret_cast<const char*>(sl) + d * 8);
+        const uint32_t* sR = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(sl) +
+                                                                d * 12);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) acc[kk] = sP[L::col(lane, kk)];
+        L::load_smem(sZ, lane, d, zu);
+        nrefs = sR[0];
+        if (lane < int(nrefs)) myref = sR[1 + lane];
+      } else {
+        uint32_t f = ld_relaxed(a.vflag + u);
+        while (f != 2u) {  // the L items' pre-final partial
+          __nanosleep(20);
+          f = ld_relaxed(a.vflag + u);
+        }
+        L::load_acc(a.epart + size_t(cb) * d, lane, d, acc);
+        L::load(a.zold + size_t(u) * d, lane, d, zu, false);
+        const uint32_t* R = a.rl + size_t(i) * kRefStride;
+        nrefs = __ldcg(R);
+        if (lane < int(nrefs)) myref = __ldcg(R + 1 + lane);
+      }
+      double lsum = (MON && lane == 0) ? __ldcg(a.eloss + cb) : 0.0;
+      Rows<KIND, K, VEC, MON, FAST>::template run<true, true>(a.fp, myref, int(nrefs), lane, d,
+                                                              a.zold, a.znew, zu, acc, lsum,
+                                                              ring);
       const uint32_t es = i - s0;
-      float* rrow = es < a.maxe ? ring + (size_t(j % RS) * a.maxe + es) * a.d : nullptr;
+      float* rrow = es < a.maxe ? ring + (size_t(j % RS) * a.maxe + es) * d : nullptr;
       finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum, rrow);
       if (lane == 0) a.vflag[u] = 0;
     }
+    __syncwarp();
+    if (j + 1 < nb) prefetch(j + 1);
     __syncthreads();  // batch j's ring rows are visible to batch j+1
   }
 }
 
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
 void launch_engine(Ctx& c, const EpochArgs& a) {
+  if constexpr (!VEC) {
+    fail(F2V_EUSAGE, "chain engine requires the vector row layout");
+  } else {
   auto kern = engine_kernel<KIND, K, VEC, MON, FAST>;
-  const size_t smem = size_t(a.Re + 1) * a.maxe * a.d * sizeof(float);
+  const size_t slot_words = (size_t(a.d) * 12 + kRefStride * 4 + 15) / 16 * 4;
+  const size_t smem = size_t(a.Re + 1) * a.maxe * a.d * sizeof(float) +
+                      size_t(kEngineWarps) * kStage * slot_words * 4;
   F2V_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   kern<<<1, kEngineWarps * 32, smem, c.stream2>>>(a);
   F2V_LAUNCHED(c.stream2, "engine_kernel");
   ++c.launches;
+  }
 }
 
 // Launch one epoch kernel instantiation as a persistent grid.

@@ -85,7 +85,7 @@ struct Ctx {
   DeviceBuf perm, state, negs_all, negwin, items, litems, nE, nL, EP, LP, wtot, needs, scan_tmp,
       epart, eloss, wcnt, wl, lpart, lloss, ploss, counters;
   uint32_t last_litems = 0;
-  DeviceBuf nEng, ecum, epos, eslot, rcnt, lrc;   // chain engine lists
+  DeviceBuf nEng, ecum, epos, eslot, eidx, rcnt;  // chain engine lists
   cudaStream_t stream2 = nullptr;                 // the chain engine runs here
   cudaEvent_t ev_prep = nullptr, ev_engine = nullptr;
   DeviceBuf trace;  // DEBUG: per-position finalise timestamps (F2V_TRACE)
