@@ -287,7 +287,7 @@ const char* f2v_last_error(const f2v_ctx* h) { return h ? h->c.err.c_str() : "";
 int32_t f2v_debug_trace(f2v_ctx* h, uint64_t* out, uint32_t* litems) {
   if (!h || !h->c.trace.p) return F2V_EUSAGE;
   if (litems) *litems = h->c.last_litems;
-  return cudaMemcpy(out, h->c.trace.p, sizeof(uint64_t) * 5 * h->c.n, cudaMemcpyDeviceToHost) ==
+  return cudaMemcpy(out, h->c.trace.p, h->c.trace.bytes, cudaMemcpyDeviceToHost) ==
                  cudaSuccess
              ? F2V_OK
              : F2V_ECUDA;

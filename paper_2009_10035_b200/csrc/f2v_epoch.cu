@@ -267,7 +267,18 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
   c.ploss.ensure(sizeof(double) * std::max<uint32_t>(n, 1));
   c.counters.ensure(64);
   const uint32_t W = c.tune.window;
-  const uint32_t Re = c.tune.erecent;  // 0: no chain engine
+  // effective engine window: 0 when the engine cannot run for this layout
+  uint32_t Re = c.tune.erecent;
+  {
+    const size_t stage = size_t(ep::kEngineWarps) * ep::kStage *
+                         ((size_t(c.d) * 12 + ep::kRefStride * 4 + 15) / 16 * 16);
+    const size_t budget = 210u * 1024u > stage ? 210u * 1024u - stage : 0;
+    c.eff_maxe = Re ? uint32_t(std::min<size_t>(64, budget / (size_t(Re + 1) * c.d * 4))) : 0u;
+    if (Re && (!c.tune.fast || c.eff_maxe < 4 || n >= kIdMask ||
+               (c.d != 64 && c.d != 128 && c.d != 256)))
+      Re = 0;
+    c.eff_re = Re;
+  }
   c.nEng.ensure(sizeof(uint32_t) * (n + 1));
   c.ecum.ensure(sizeof(uint32_t) * (n + 1));
   c.epos.ensure(sizeof(uint4) * std::max<uint32_t>(n, 1));
@@ -376,21 +387,13 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.W = c.tune.window;
   a.R = c.tune.recent;
   a.lwarps = c.tune.lwarps;
-  a.Re = c.tune.erecent;
   a.rl = c.rcnt.as<uint32_t>();
   a.erec = c.epos.as<uint4>();
   a.ecum = c.ecum.as<uint32_t>();
   a.eslot = c.eslot.as<uint32_t>();
   a.eidx = c.eidx.as<uint32_t>();
-  {  // ring rows per batch: what is left of ~210 KB after the engine's staging area
-    const size_t stage = size_t(ep::kEngineWarps) * ep::kStage *
-                         ((size_t(c.d) * 12 + ep::kRefStride * 4 + 15) / 16 * 16);
-    const size_t budget = 210u * 1024u > stage ? 210u * 1024u - stage : 0;
-    a.maxe = a.Re ? uint32_t(std::min<size_t>(64, budget / (size_t(a.Re + 1) * c.d * 4))) : 0u;
-  }
-  // no engine for rows too wide for a ring, huge n, or the masked row layouts
-  if (a.Re && (a.maxe < 4 || c.n >= kIdMask || (c.d != 64 && c.d != 128 && c.d != 256)))
-    a.Re = 0;
+  a.Re = c.eff_re;  // decided by the prep (0: no engine this epoch)
+  a.maxe = c.eff_maxe;
   a.eta = eta;
   a.fp = fp;
   a.nodep = std::getenv("F2V_DEBUG_NODEP") ? 1 : 0;
@@ -399,11 +402,15 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.lslots = c.lslots;
   a.trace = nullptr;
   a.ltrace = nullptr;
+  a.etrace = nullptr;
   if (std::getenv("F2V_TRACE")) {
-    c.trace.ensure(sizeof(unsigned long long) * 5 * std::max<uint32_t>(c.n, 1));
+    const uint32_t nbt = (c.n + b - 1) / b;
+    c.trace.ensure(sizeof(unsigned long long) * (5ull * std::max<uint32_t>(c.n, 1) + 3ull * nbt));
     a.trace = c.trace.as<unsigned long long>();
     a.ltrace = a.trace + c.n;
-    F2V_CUDA(cudaMemsetAsync(a.ltrace, 0, sizeof(unsigned long long) * 4 * c.n, c.stream));
+    a.etrace = a.ltrace + 4ull * c.n;
+    F2V_CUDA(cudaMemsetAsync(a.ltrace, 0, sizeof(unsigned long long) * (4ull * c.n + 3ull * nbt),
+                             c.stream));
   }
   if (!c.ev_kernel.size()) {
     c.ev_kernel.resize(2);

@@ -72,6 +72,7 @@ struct EpochArgs {
   int nodep;                    // DEBUG (F2V_DEBUG_NODEP): every row read from Zold, no waits
   unsigned long long* trace;    // DEBUG (F2V_TRACE): per position finalise time (ns)
   unsigned long long* ltrace;   // DEBUG (F2V_TRACE): per position L-item stage times (4 x ns)
+  unsigned long long* etrace;   // DEBUG (F2V_TRACE): engine per batch [start, computed, staged]
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -578,6 +579,7 @@ __global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs 
   for (uint32_t j = 0; j < nb; ++j) {
     uint32_t s0, s1;
     range(j, s0, s1);
+    if (a.etrace && threadIdx.x == 0) a.etrace[3ull * j] = globaltimer();
     cp_async_wait_all();
     __syncwarp();
     int k = 0;
@@ -621,8 +623,10 @@ __global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs 
       if (lane == 0) a.vflag[u] = 0;
     }
     __syncwarp();
+    if (a.etrace && lane == 0) atomicMax(a.etrace + 3ull * j + 1, globaltimer());
     if (j + 1 < nb) prefetch(j + 1);
     __syncthreads();  // batch j's ring rows are visible to batch j+1
+    if (a.etrace && threadIdx.x == 0) a.etrace[3ull * j + 2] = globaltimer();
   }
 }
 

@@ -88,6 +88,7 @@ struct Ctx {
   DeviceBuf nEng, ecum, epos, eslot, eidx, rcnt;  // chain engine lists
   cudaStream_t stream2 = nullptr;                 // the chain engine runs here
   cudaEvent_t ev_prep = nullptr, ev_engine = nullptr;
+  uint32_t eff_re = 0, eff_maxe = 0;              // engine window / ring rows this epoch
   DeviceBuf trace;  // DEBUG: per-position finalise timestamps (F2V_TRACE)
   DeviceBuf shufR, shufL;  // device Fisher-Yates (f2v_perm.cu)
 

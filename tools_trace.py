@@ -15,9 +15,11 @@ cfg = f2v.TrainConfig(dim=128, batch=b, negatives=5, lr=0.02, epochs=4,
 for e in range(3):
     dev.train_epochs(cfg, e, 1)
     t = dev.last_timing()
-tr = np.zeros(5 * n, np.uint64); nl = C.c_uint32()
+nbt = (n + b - 1) // b
+tr = np.zeros(5 * n + 3 * nbt, np.uint64); nl = C.c_uint32()
 lib.f2v_debug_trace(dev._h, tr, C.byref(nl))
-fin = tr[:n].astype(np.float64); lt = tr[n:].reshape(n, 4).astype(np.float64)
+fin = tr[:n].astype(np.float64); lt = tr[n:5*n].reshape(n, 4).astype(np.float64)
+et = tr[5*n:].reshape(nbt, 3).astype(np.float64)
 t0 = fin.min(); fin = (fin - t0) / 1e3
 has = lt[:, 0] > 0
 lt[has] = (lt[has] - t0) / 1e3
@@ -50,3 +52,9 @@ print("old+negs done - prev_done:", pc(lt[c2, 2] - pd))
 print("recent done - prev_done:", pc(lt[c2, 3] - pd))
 print("final - prev_done:", pc(fin[c2] - pd))
 print("final - recent done:", pc(fin[c2] - lt[c2, 3]))
+
+if et[:, 0].max() > 0:
+    et = (et - t0) / 1e3
+    comp = et[:, 1] - et[:, 0]; tail = et[:, 2] - et[:, 1]; step = np.diff(et[:, 0])
+    print("ENGINE step us: mean %.2f median %.2f p90 %.2f | compute median %.2f p90 %.2f | prefetch+barrier median %.2f" % (step.mean(), np.median(step), np.percentile(step, 90), np.median(comp), np.percentile(comp, 90), np.median(tail)))
+    print("engine total ms %.2f; first step at %.1f us" % ((et[-1, 2] - et[0, 0]) / 1e3, et[0, 0]))
