@@ -405,12 +405,12 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.etrace = nullptr;
   if (std::getenv("F2V_TRACE")) {
     const uint32_t nbt = (c.n + b - 1) / b;
-    c.trace.ensure(sizeof(unsigned long long) * (5ull * std::max<uint32_t>(c.n, 1) + 3ull * nbt));
+    c.trace.ensure(sizeof(unsigned long long) * (5ull * std::max<uint32_t>(c.n, 1) + 3ull * nbt + 2));
     a.trace = c.trace.as<unsigned long long>();
     a.ltrace = a.trace + c.n;
     a.etrace = a.ltrace + 4ull * c.n;
-    F2V_CUDA(cudaMemsetAsync(a.ltrace, 0, sizeof(unsigned long long) * (4ull * c.n + 3ull * nbt),
-                             c.stream));
+    F2V_CUDA(cudaMemsetAsync(a.ltrace, 0,
+                             sizeof(unsigned long long) * (4ull * c.n + 3ull * nbt + 2), c.stream));
   }
   if (!c.ev_kernel.size()) {
     c.ev_kernel.resize(2);

@@ -541,50 +541,47 @@ __global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs 
   const size_t slot_words = (size_t(d) * 12 + kRefStride * 4 + 15) / 16 * 4;
   uint32_t* stage = reinterpret_cast<uint32_t*>(ring + size_t(RS) * a.maxe * d) +
                     size_t(w) * kStage * slot_words;
+  // records of this warp's first kStage vertices, three batches in flight
+  __shared__ uint4 srec[3][kEngineWarps][kStage];
   __shared__ uint32_t staged[kEngineWarps][kStage];
   const uint32_t nb = (a.n + a.b - 1) / a.b;
-
-  auto range = [&](uint32_t j, uint32_t& s0, uint32_t& s1) {
-    s0 = __ldg(a.ecum + umin64(uint64_t(j) * a.b, a.n));
-    s1 = __ldg(a.ecum + umin64(uint64_t(j + 1) * a.b, a.n));
-  };
-  // stage P, z_u and the refs of this warp's first kStage vertices of batch j
-  auto prefetch = [&](uint32_t j) {
-    uint32_t s0, s1;
-    range(j, s0, s1);
-    for (int k = 0; k < kStage; ++k) {
-      const uint32_t i = s0 + w + uint32_t(k) * kEngineWarps;
-      uint32_t ok = 0;
-      if (i < s1) {
-        const uint4 rec = __ldg(a.erec + i);
-        ok = ld_relaxed(a.vflag + rec.x) == 2u;
-        if (ok) {
-          uint32_t* sl = stage + size_t(k) * slot_words;
-          const char* P = reinterpret_cast<const char*>(a.epart + size_t(rec.y) * d);
-          const char* Z = reinterpret_cast<const char*>(a.zold + size_t(rec.x) * d);
-          const char* R = reinterpret_cast<const char*>(a.rl + size_t(i) * kRefStride);
-          char* dst = reinterpret_cast<char*>(sl);
-          for (uint32_t off = lane * 16; off < d * 8; off += 512) cp_async16(dst + off, P + off);
-          for (uint32_t off = lane * 16; off < d * 4; off += 512)
-            cp_async16(dst + d * 8 + off, Z + off);
-          if (lane * 16 < kRefStride * 4) cp_async16(dst + d * 12 + lane * 16, R + lane * 16);
-        }
-      }
-      if (lane == 0) staged[w][k] = ok;
+  auto cum = [&](uint32_t j) { return __ldg(a.ecum + umin64(uint64_t(j) * a.b, a.n)); };
+  // lane k < kStage: request the record of slot k of batch jj (cp.async, 16 bytes)
+  auto fetch_rec = [&](uint32_t jj, uint32_t e0, uint32_t e1) {
+    const uint32_t i = e0 + w + uint32_t(lane) * kEngineWarps;
+    if (lane < kStage) {
+      if (i < e1) cp_async16(&srec[jj % 3][w][lane], a.erec + i);
+      else srec[jj % 3][w][lane] = make_uint4(0xffffffffu, 0, 0, 0);
     }
-    cp_async_commit();
   };
-
-  prefetch(0);
+  uint32_t c0 = cum(0), c1 = cum(1), c2 = cum(2), c3 = cum(3);
+  fetch_rec(0, c0, c1);
+  fetch_rec(1, c1, c2);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncwarp();
+  if (lane < kStage) staged[w][lane] = 0;  // batch 0: nothing staged
+  __syncwarp();
+  uint32_t waits = 0;
+  unsigned long long wait_ns = 0;
   for (uint32_t j = 0; j < nb; ++j) {
-    uint32_t s0, s1;
-    range(j, s0, s1);
     if (a.etrace && threadIdx.x == 0) a.etrace[3ull * j] = globaltimer();
-    cp_async_wait_all();
-    __syncwarp();
+    // (a) records of batch j+2; (b) readiness of batch j+1's staged slots (non-blocking)
+    const uint32_t c4 = j + 4 <= nb ? cum(j + 4) : c3;
+    if (j + 2 < nb) fetch_rec(j + 2, c2, c3);
+    cp_async_commit();
+    uint32_t ready = 0;
+    uint4 nrec = make_uint4(0xffffffffu, 0, 0, 0);
+    if (lane < kStage && j + 1 < nb) {
+      nrec = srec[(j + 1) % 3][w][lane];
+      if (nrec.x != 0xffffffffu) ready = ld_relaxed(a.vflag + nrec.x) == 2u;
+    }
+    // (c) this batch's vertices
     int k = 0;
-    for (uint32_t i = s0 + w; i < s1; i += kEngineWarps, ++k) {
-      const uint4 rec = __ldg(a.erec + i);
+    for (uint32_t i = c0 + w; i < c1; i += kEngineWarps, ++k) {
+      uint4 rec;
+      if (k < kStage) rec = srec[j % 3][w][k];
+      else rec = __ldg(a.erec + i);
       const uint32_t u = rec.x, cb = rec.y, p = rec.z;
       float zu[K];
       double acc[K];
@@ -602,10 +599,15 @@ __global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs 
         nrefs = sR[0];
         if (lane < int(nrefs)) myref = sR[1 + lane];
       } else {
+        const unsigned long long t0 = a.etrace ? globaltimer() : 0ull;
         uint32_t f = ld_relaxed(a.vflag + u);
         while (f != 2u) {  // the L items' pre-final partial
           __nanosleep(20);
           f = ld_relaxed(a.vflag + u);
+        }
+        if (a.etrace) {
+          ++waits;
+          wait_ns += globaltimer() - t0;
         }
         L::load_acc(a.epart + size_t(cb) * d, lane, d, acc);
         L::load(a.zold + size_t(u) * d, lane, d, zu, false);
@@ -617,16 +619,42 @@ __global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs 
       Rows<KIND, K, VEC, MON, FAST>::template run<true, true>(a.fp, myref, int(nrefs), lane, d,
                                                               a.zold, a.znew, zu, acc, lsum,
                                                               ring);
-      const uint32_t es = i - s0;
+      const uint32_t es = i - c0;
       float* rrow = es < a.maxe ? ring + (size_t(j % RS) * a.maxe + es) * d : nullptr;
       finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum, rrow);
       if (lane == 0) a.vflag[u] = 0;
     }
-    __syncwarp();
     if (a.etrace && lane == 0) atomicMax(a.etrace + 3ull * j + 1, globaltimer());
-    if (j + 1 < nb) prefetch(j + 1);
+    // (d) stage batch j+1's ready vertices
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < kStage; ++kk) {
+      const uint32_t ok = __shfl_sync(kFull, ready, kk);
+      const uint32_t u = __shfl_sync(kFull, nrec.x, kk), cb = __shfl_sync(kFull, nrec.y, kk);
+      const uint32_t i = c1 + w + uint32_t(kk) * kEngineWarps;
+      if (ok) {
+        char* dst = reinterpret_cast<char*>(stage + size_t(kk) * slot_words);
+        const char* P = reinterpret_cast<const char*>(a.epart + size_t(cb) * d);
+        const char* Z = reinterpret_cast<const char*>(a.zold + size_t(u) * d);
+        const char* R = reinterpret_cast<const char*>(a.rl + size_t(i) * kRefStride);
+        for (uint32_t off = lane * 16; off < d * 8; off += 512) cp_async16(dst + off, P + off);
+        for (uint32_t off = lane * 16; off < d * 4; off += 512) cp_async16(dst + d * 8 + off, Z + off);
+        if (lane * 16 < kRefStride * 4) cp_async16(dst + d * 12 + lane * 16, R + lane * 16);
+      }
+      if (lane == 0) staged[w][kk] = ok;
+    }
+    cp_async_commit();
+    cp_async_wait_all();
     __syncthreads();  // batch j's ring rows are visible to batch j+1
     if (a.etrace && threadIdx.x == 0) a.etrace[3ull * j + 2] = globaltimer();
+    c0 = c1;
+    c1 = c2;
+    c2 = c3;
+    c3 = c4;
+  }
+  if (a.etrace && lane == 0 && waits) {
+    atomicAdd(a.etrace + 3ull * nb, (unsigned long long)waits);
+    atomicAdd(a.etrace + 3ull * nb + 1, wait_ns);
   }
 }
 

@@ -16,10 +16,11 @@ for e in range(3):
     dev.train_epochs(cfg, e, 1)
     t = dev.last_timing()
 nbt = (n + b - 1) // b
-tr = np.zeros(5 * n + 3 * nbt, np.uint64); nl = C.c_uint32()
+tr = np.zeros(5 * n + 3 * nbt + 2, np.uint64); nl = C.c_uint32()
 lib.f2v_debug_trace(dev._h, tr, C.byref(nl))
 fin = tr[:n].astype(np.float64); lt = tr[n:5*n].reshape(n, 4).astype(np.float64)
-et = tr[5*n:].reshape(nbt, 3).astype(np.float64)
+et = tr[5*n:5*n+3*nbt].reshape(nbt, 3).astype(np.float64)
+print('engine unstaged waits', int(tr[-2]), 'wait ms', tr[-1] / 1e6)
 t0 = fin.min(); fin = (fin - t0) / 1e3
 has = lt[:, 0] > 0
 lt[has] = (lt[has] - t0) / 1e3
