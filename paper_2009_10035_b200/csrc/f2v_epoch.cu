@@ -270,7 +270,7 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
   // effective engine window: 0 when the engine cannot run for this layout
   uint32_t Re = c.tune.erecent;
   {
-    const size_t stage = size_t(ep::kEngineWarps) * ep::kStage *
+    const size_t stage = 2 * size_t(ep::kEngineWarps) * ep::kStage *
                          ((size_t(c.d) * 12 + ep::kRefStride * 4 + 15) / 16 * 16);
     const size_t budget = 210u * 1024u > stage ? 210u * 1024u - stage : 0;
     c.eff_maxe = Re ? uint32_t(std::min<size_t>(64, budget / (size_t(Re + 1) * c.d * 4))) : 0u;

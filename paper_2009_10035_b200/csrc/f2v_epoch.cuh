@@ -435,6 +435,7 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
       __threadfence();
       __syncwarp();
       if (lane == 0) st_relaxed(a.vflag + u, 2u);
+      if (lt && lane == 0) lt[2] = globaltimer();
       return;
     }
     // E total + old window arcs + negatives + recent arcs
@@ -514,8 +515,8 @@ __global__ void __launch_bounds__(kWarps * 32, 2) epoch_kernel(EpochArgs a) {
 // round trips.  P(u) and z_u of the next batch are staged into shared memory
 // with cp.async while the current batch computes.  Batch j's ring rows are
 // reused at batch j+Re+1.
-constexpr int kEngineWarps = 16;
-constexpr int kStage = 3;  // staged vertices per warp per batch
+constexpr int kEngineWarps = 8;
+constexpr int kStage = 2;  // staged vertices per warp per batch (x2 buffers)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t sa = uint32_t(__cvta_generic_to_shared(smem));
@@ -526,6 +527,10 @@ __device__ __forceinline__ void cp_async_commit() {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
@@ -541,54 +546,91 @@ __global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs 
   const size_t slot_words = (size_t(d) * 12 + kRefStride * 4 + 15) / 16 * 4;
   uint32_t* stage = reinterpret_cast<uint32_t*>(ring + size_t(RS) * a.maxe * d) +
                     size_t(w) * kStage * slot_words;
-  // records of this warp's first kStage vertices, three batches in flight
-  __shared__ uint4 srec[3][kEngineWarps][kStage];
-  __shared__ uint32_t staged[kEngineWarps][kStage];
+  // records of this warp's first kStage vertices, four batches in flight;
+  // staging is double-buffered and filled two batches ahead
+  __shared__ uint4 srec[4][kEngineWarps][kStage];
+  __shared__ uint32_t staged[2][kEngineWarps][kStage];
   const uint32_t nb = (a.n + a.b - 1) / a.b;
   auto cum = [&](uint32_t j) { return __ldg(a.ecum + umin64(uint64_t(j) * a.b, a.n)); };
+  auto slotp = [&](uint32_t buf, int k) {
+    return stage + (size_t(buf) * kStage + k) * slot_words;
+  };
   // lane k < kStage: request the record of slot k of batch jj (cp.async, 16 bytes)
   auto fetch_rec = [&](uint32_t jj, uint32_t e0, uint32_t e1) {
-    const uint32_t i = e0 + w + uint32_t(lane) * kEngineWarps;
     if (lane < kStage) {
-      if (i < e1) cp_async16(&srec[jj % 3][w][lane], a.erec + i);
-      else srec[jj % 3][w][lane] = make_uint4(0xffffffffu, 0, 0, 0);
+      const uint32_t i = e0 + w + uint32_t(lane) * kEngineWarps;
+      if (jj < nb && i < e1) cp_async16(&srec[jj % 4][w][lane], a.erec + i);
+      else srec[jj % 4][w][lane] = make_uint4(0xffffffffu, 0, 0, 0);
     }
   };
-  uint32_t c0 = cum(0), c1 = cum(1), c2 = cum(2), c3 = cum(3);
+  // stage batch jj's ready slots (lane k < kStage holds slot k's readiness + record)
+  auto stage_batch = [&](uint32_t jj, uint32_t e0, uint32_t ready, uint4 r) {
+#pragma unroll
+    for (int kk = 0; kk < kStage; ++kk) {
+      const uint32_t ok = __shfl_sync(kFull, ready, kk);
+      const uint32_t u = __shfl_sync(kFull, r.x, kk), cb = __shfl_sync(kFull, r.y, kk);
+      const uint32_t i = e0 + w + uint32_t(kk) * kEngineWarps;
+      if (ok) {
+        char* dst = reinterpret_cast<char*>(slotp(jj & 1, kk));
+        const char* P = reinterpret_cast<const char*>(a.epart + size_t(cb) * d);
+        const char* Z = reinterpret_cast<const char*>(a.zold + size_t(u) * d);
+        const char* R = reinterpret_cast<const char*>(a.rl + size_t(i) * kRefStride);
+        for (uint32_t off = lane * 16; off < d * 8; off += 512) cp_async16(dst + off, P + off);
+        for (uint32_t off = lane * 16; off < d * 4; off += 512)
+          cp_async16(dst + d * 8 + off, Z + off);
+        if (lane * 16 < kRefStride * 4) cp_async16(dst + d * 12 + lane * 16, R + lane * 16);
+      }
+      if (lane == 0) staged[jj & 1][w][kk] = ok;
+    }
+  };
+  // prologue: records of batches 0..2, staging of batches 0 and 1
+  uint32_t c0 = cum(0), c1 = cum(1), c2 = cum(2), c3 = cum(3), c4 = cum(4);
   fetch_rec(0, c0, c1);
   fetch_rec(1, c1, c2);
+  fetch_rec(2, c2, c3);
   cp_async_commit();
   cp_async_wait_all();
   __syncwarp();
-  if (lane < kStage) staged[w][lane] = 0;  // batch 0: nothing staged
-  __syncwarp();
+  for (uint32_t jj = 0; jj < 2; ++jj) {
+    uint32_t ready = 0;
+    uint4 r = make_uint4(0xffffffffu, 0, 0, 0);
+    if (lane < kStage) {
+      r = srec[jj % 4][w][lane];
+      if (r.x != 0xffffffffu) ready = ld_relaxed(a.vflag + r.x) == 2u;
+    }
+    stage_batch(jj, jj == 0 ? c0 : c1, ready, r);
+  }
+  cp_async_commit();
   uint32_t waits = 0;
   unsigned long long wait_ns = 0;
   for (uint32_t j = 0; j < nb; ++j) {
     if (a.etrace && threadIdx.x == 0) a.etrace[3ull * j] = globaltimer();
-    // (a) records of batch j+2; (b) readiness of batch j+1's staged slots (non-blocking)
-    const uint32_t c4 = j + 4 <= nb ? cum(j + 4) : c3;
-    if (j + 2 < nb) fetch_rec(j + 2, c2, c3);
+    // every group but the newest (batch j+1's staging) has landed: batch j's staging
+    // and batch j+2's records
+    cp_async_wait_group<1>();
+    __syncwarp();
+    fetch_rec(j + 3, c3, c4);
     cp_async_commit();
+    const uint32_t c5 = j + 5 <= nb ? cum(j + 5) : c4;
     uint32_t ready = 0;
     uint4 nrec = make_uint4(0xffffffffu, 0, 0, 0);
-    if (lane < kStage && j + 1 < nb) {
-      nrec = srec[(j + 1) % 3][w][lane];
+    if (lane < kStage && j + 2 < nb) {  // readiness of batch j+2 (non-blocking load)
+      nrec = srec[(j + 2) % 4][w][lane];
       if (nrec.x != 0xffffffffu) ready = ld_relaxed(a.vflag + nrec.x) == 2u;
     }
-    // (c) this batch's vertices
     int k = 0;
     for (uint32_t i = c0 + w; i < c1; i += kEngineWarps, ++k) {
       uint4 rec;
-      if (k < kStage) rec = srec[j % 3][w][k];
+      if (k < kStage) rec = srec[j % 4][w][k];
       else rec = __ldg(a.erec + i);
       const uint32_t u = rec.x, cb = rec.y, p = rec.z;
+      if (a.ltrace && lane == 0) a.ltrace[4ull * p + 3] = globaltimer();
       float zu[K];
       double acc[K];
       uint32_t nrefs, myref = 0;
-      const bool st = k < kStage && staged[w][k];
+      const bool st = k < kStage && staged[j & 1][w][k];
       if (st) {
-        const uint32_t* sl = stage + size_t(k) * slot_words;
+        const uint32_t* sl = slotp(j & 1, k);
         const double* sP = reinterpret_cast<const double*>(sl);
         const float* sZ = reinterpret_cast<const float*>(reinterpret_cast<const char*>(sl) + d * 8);
         const uint32_t* sR = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(sl) +
@@ -625,33 +667,18 @@ __global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs 
       if (lane == 0) a.vflag[u] = 0;
     }
     if (a.etrace && lane == 0) atomicMax(a.etrace + 3ull * j + 1, globaltimer());
-    // (d) stage batch j+1's ready vertices
     __syncwarp();
-#pragma unroll
-    for (int kk = 0; kk < kStage; ++kk) {
-      const uint32_t ok = __shfl_sync(kFull, ready, kk);
-      const uint32_t u = __shfl_sync(kFull, nrec.x, kk), cb = __shfl_sync(kFull, nrec.y, kk);
-      const uint32_t i = c1 + w + uint32_t(kk) * kEngineWarps;
-      if (ok) {
-        char* dst = reinterpret_cast<char*>(stage + size_t(kk) * slot_words);
-        const char* P = reinterpret_cast<const char*>(a.epart + size_t(cb) * d);
-        const char* Z = reinterpret_cast<const char*>(a.zold + size_t(u) * d);
-        const char* R = reinterpret_cast<const char*>(a.rl + size_t(i) * kRefStride);
-        for (uint32_t off = lane * 16; off < d * 8; off += 512) cp_async16(dst + off, P + off);
-        for (uint32_t off = lane * 16; off < d * 4; off += 512) cp_async16(dst + d * 8 + off, Z + off);
-        if (lane * 16 < kRefStride * 4) cp_async16(dst + d * 12 + lane * 16, R + lane * 16);
-      }
-      if (lane == 0) staged[w][kk] = ok;
-    }
+    if (j + 2 < nb) stage_batch(j + 2, c2, ready, nrec);  // into buffer (j & 1), now free
     cp_async_commit();
-    cp_async_wait_all();
     __syncthreads();  // batch j's ring rows are visible to batch j+1
     if (a.etrace && threadIdx.x == 0) a.etrace[3ull * j + 2] = globaltimer();
     c0 = c1;
     c1 = c2;
     c2 = c3;
     c3 = c4;
+    c4 = c5;
   }
+  cp_async_wait_all();
   if (a.etrace && lane == 0 && waits) {
     atomicAdd(a.etrace + 3ull * nb, (unsigned long long)waits);
     atomicAdd(a.etrace + 3ull * nb + 1, wait_ns);
@@ -666,7 +693,7 @@ void launch_engine(Ctx& c, const EpochArgs& a) {
   auto kern = engine_kernel<KIND, K, VEC, MON, FAST>;
   const size_t slot_words = (size_t(a.d) * 12 + kRefStride * 4 + 15) / 16 * 4;
   const size_t smem = size_t(a.Re + 1) * a.maxe * a.d * sizeof(float) +
-                      size_t(kEngineWarps) * kStage * slot_words * 4;
+                      2 * size_t(kEngineWarps) * kStage * slot_words * 4;
   F2V_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   kern<<<1, kEngineWarps * 32, smem, c.stream2>>>(a);
   F2V_LAUNCHED(c.stream2, "engine_kernel");
