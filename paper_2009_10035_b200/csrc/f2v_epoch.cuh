@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs 
   // staging: per warp kStage slots of [P (d doubles) | z_u (d floats) | refs (kRefStride words)]
   const size_t slot_words = (size_t(d) * 12 + kRefStride * 4 + 15) / 16 * 4;
   uint32_t* stage = reinterpret_cast<uint32_t*>(ring + size_t(RS) * a.maxe * d) +
-                    size_t(w) * kStage * slot_words;
+                    size_t(w) * 2 * kStage * slot_words;  // two buffers per warp
   // records of this warp's first kStage vertices, four batches in flight;
   // staging is double-buffered and filled two batches ahead
   __shared__ uint4 srec[4][kEngineWarps][kStage];
