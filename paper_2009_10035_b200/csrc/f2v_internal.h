@@ -50,7 +50,7 @@ struct EpochTuning {
   uint32_t recent = 2;   // F2V_RECENT: window arcs this recent are taken last
   uint32_t lwarps = 2;   // F2V_LWARPS: L-role warps per 8-warp CTA
   uint32_t fast = 1;     // F2V_PRECISION=exact|fast: pair math precision (config)
-  uint32_t erecent = 8;  // F2V_ERECENT: chain engine takes arcs of age <= this (0 = off)
+  uint32_t erecent = 0;  // F2V_ERECENT: chain engine takes arcs of age <= this (0 = off; opt-in)
 };
 void load_tuning(EpochTuning& t);
 
