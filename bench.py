@@ -26,6 +26,7 @@ Printed JSON (rank 0, one line):
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import subprocess
@@ -268,9 +269,19 @@ def bench_b200(args):
                           epochs=args.warmup + args.steps,
                           model=f2v.ForceModel(f2v.ForceKind.parse(kind)), seed=1,
                           monitor_loss=False, sampler="philox")
-    dev = f2v.Device(local)
-    dev.upload_graph(g)
-    dev.uniform_embedding(n, d, 1, -1.0, 1.0)  # the configs' U(-1,1) from Rng(seed, 0)
+    if world > 1:
+        # vertex-partitioned shards: each GPU runs its
+        # rows and stores every updated row into all replicas over NVLink
+        from paper_2009_10035_b200.dist import ShardedDevice
+        sd = ShardedDevice(rank, world, local)
+        sd.setup(g, dim=d, seed=1)  # the configs' U(-1,1) from Rng(seed, 0)
+        dev = sd.dev
+        cfg = dataclasses.replace(cfg, shards=world)
+    else:
+        sd = None
+        dev = f2v.Device(local)
+        dev.upload_graph(g)
+        dev.uniform_embedding(n, d, 1, -1.0, 1.0)  # the configs' U(-1,1) from Rng(seed, 0)
     dev.train_epochs(cfg, 0, args.warmup)  # untimed warm-up epochs
     if world > 1:
         import torch.distributed as dist
@@ -287,23 +298,31 @@ def bench_b200(args):
     if world > 1:
         import torch
         import torch.distributed as dist
-        tt = torch.tensor([dev_ms], device=f"cuda:{local}")
+        tt = torch.tensor([dev_ms, kern_ms], device=f"cuda:{local}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dev_ms = float(tt.item())
+        dev_ms, kern_ms = float(tt[0].item()), float(tt[1].item())
     z = dev.get_embedding()
     assert np.all(np.isfinite(z)), "non-finite embedding"
     pairs = nnz + n * s
-    value = world * pairs * args.steps / (dev_ms / 1e3)
+    # the G shards split ONE epoch of the whole graph: total work is fixed
+    value = pairs * args.steps / (dev_ms / 1e3)
     ms_per_step = dev_ms / args.steps
     algo = algorithmic_bytes(n, nnz, d, min(b, n), s)
     peak, peak_kind = hbm_peak()
     achieved = algo / (kern_ms / nk / 1e3) / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(cfg_name),
-            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
+            "frac": achieved / (peak * world), "traffic": ncu_traffic(cfg_name) if world == 1
+            else None,
+            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" + (
+                f" x {world} GPUs" if world > 1 else "") if peak_kind == "measured"
             else "fallback 6650 GB/s (B200_PROFILING.md)",
             "algorithmic_bytes_per_launch": algo,
             "kernel_ms_per_launch": kern_ms / nk}
+    if world > 1:  # the fused row exchange: every GPU stores its rows into G-1 replicas
+        xbytes = (world - 1) * (n // world) * 4 * d
+        roof["nvlink"] = {"bytes_per_gpu_per_epoch": xbytes,
+                          "achieved_GBps": xbytes / (kern_ms / nk / 1e3) / 1e9,
+                          "peak_GBps": 900.0, "peak_source": "NVLink 5 nominal per direction"}
     # ------------------------------------------------------------ e2e
     import torch
     h_row = torch.from_numpy(g.row_offsets).pin_memory().numpy()
@@ -318,7 +337,18 @@ def bench_b200(args):
     cfg_e2e = f2v.TrainConfig(dim=d, batch=b, negatives=s, lr=lr, epochs=epochs,
                               model=cfg.model, seed=1, monitor_loss=False, sampler="philox")
 
+    if world > 1:
+        cfg_e2e = dataclasses.replace(cfg_e2e, shards=world)
+
     def e2e_once():
+        if world > 1:  # the public sharded API, from host buffers
+            s2 = ShardedDevice(rank, world, local)
+            s2.setup(g_pinned, h_z0)
+            s2.train_epochs(cfg_e2e)
+            out = np.ascontiguousarray(h_z)
+            f2v._lib.f2v_get_embedding(s2.dev._h, out)
+            s2.close()
+            return out
         dev.upload_graph(g_pinned)
         dev.set_embedding(h_z0)
         dev.train_epochs(cfg_e2e, 0, 0)
@@ -326,11 +356,17 @@ def bench_b200(args):
         f2v._lib.f2v_get_embedding(dev._h, out)
         return out
     e2e_once()  # warm
+    if world > 1:
+        dist.barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_once()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_val = world * pairs * epochs / e2e_s
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_val = pairs * epochs / e2e_s
     h2d = h_row.nbytes + h_col.nbytes + h_z0.nbytes + 4 * n * epochs  # + perms
     d2h = h_z.nbytes
     dev.close()
@@ -340,10 +376,12 @@ def bench_b200(args):
         "metric": "edge+neg-sample updates/sec (d=128)" if d == 128 else
         "edge+neg-sample updates/sec", "value": value, "unit": "updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD_NAMES[cfg_name], "n": n, "nnz": nnz, "batch": b,
                    "negatives": s, "epochs_schedule": epochs, "sampler": "philox",
+                   "parallelism": f"vertex-partitioned shards x{world} (NVLink row stores)"
+                   if world > 1 else "1 GPU",
                    "step": "one epoch (all batches) of train()",
                    "l2": "inputs larger than L2 (Z 2x%d MB + CSR %d MB > 126 MB)" %
                          (n * d * 4 >> 20, (nnz * 4 + n * 8) >> 20)},

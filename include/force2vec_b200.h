@@ -75,6 +75,13 @@ typedef struct {
   uint32_t first_epoch;  /* run epochs [first_epoch, first_epoch + run_epochs) of the */
   uint32_t run_epochs;   /* `epochs`-long schedule; run_epochs 0 = through the end */
   int32_t precision;     /* F2V_PRECISION_FAST (default) or F2V_PRECISION_EXACT */
+  uint32_t shards;       /* vertex shards G (0/1: the reference's single stream).  G > 1 =
+                            the multi-GPU semantics: shard g owns
+                            rows [n g/G, n (g+1)/G), shuffles them with (seed,{0x22,epoch,g}),
+                            and step t = every shard's t-th batch on one snapshot.  On a
+                            context attached to peers (f2v_shard_attach) G = the world
+                            size and each GPU runs its own shard; otherwise one GPU runs
+                            all G shards (same results). */
 } f2v_train_config;
 
 /* TrainCounters, trainer.hpp:83-87 */
@@ -189,6 +196,36 @@ int32_t f2v_gen_chung_lu(uint32_t n, double exponent, double min_deg, double max
 int32_t f2v_gen_rgg(uint32_t n, double mean_deg, uint64_t seed, uint32_t** pairs_out,
                     uint64_t* m_out);
 void f2v_free(void* p);
+
+/* ------------------------------------- multi-GPU (vertex-partitioned shards)
+ * No reference counterpart: the reference is single-process;
+ * the semantics are the G-shard synchronous minibatch SGD the oracle pins
+ * (orc_train with G > 1).  One process per GPU:
+ *   f2v_upload_graph + f2v_set_embedding (same Z on every rank)
+ *   f2v_shard_init(rank, world)      -- fixes both replica buffers
+ *   f2v_shard_export(handles)        -- f2v_shard_handle_bytes() bytes
+ *   (all-gather the handles across ranks, e.g. torch.distributed)
+ *   f2v_shard_attach(all_handles)    -- world * f2v_shard_handle_bytes()
+ *   f2v_train_epochs(cfg)            -- every rank, same cfg; each GPU runs its
+ *                                       rows and stores every updated row into
+ *                                       all replicas over NVLink.
+ * Host-only helpers (no GPU needed): */
+/* combined step-major layout: poff_out[t*G + g] = first position of shard g's
+ * batch t, poff_out[T*G] = n (poff_out nullable: *steps_out = T only) */
+int32_t f2v_shard_layout(uint32_t n, uint32_t batch, uint32_t shards, uint32_t* poff_out,
+                         uint32_t* steps_out);
+/* partition_epoch (sampling.cpp:7-19) of one shard's n rows, keyed
+ * (seed,{0x22,epoch}) when shards == 1 else (seed,{0x22,epoch,shard}) */
+int32_t f2v_partition_shard(uint32_t n, uint32_t b, uint64_t seed, uint32_t epoch,
+                            uint32_t shard, uint32_t shards, uint32_t* perm_out);
+int32_t f2v_shard_handle_bytes(void);
+int32_t f2v_shard_init(f2v_ctx* ctx, uint32_t rank, uint32_t world);
+int32_t f2v_shard_export(f2v_ctx* ctx, uint8_t* handles_out);
+int32_t f2v_shard_attach(f2v_ctx* ctx, const uint8_t* all_handles);
+/* rows of the device Z by id (the per-step all-gather driver, dist.py):
+ * rows f32[b*d] row-major */
+int32_t f2v_get_rows(f2v_ctx* ctx, const uint32_t* ids, uint32_t b, float* rows_out);
+int32_t f2v_set_rows(f2v_ctx* ctx, const uint32_t* ids, uint32_t b, const float* rows);
 
 #ifdef __cplusplus
 }

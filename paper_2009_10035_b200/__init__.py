@@ -83,7 +83,7 @@ class _TrainConfig(C.Structure):
                 ("lr", C.c_float), ("epochs", C.c_uint32), ("model", _ForceModel),
                 ("seed", C.c_uint64), ("lr_decay", C.c_int32), ("monitor_loss", C.c_int32),
                 ("sampler", C.c_int32), ("init", C.c_int32), ("first_epoch", C.c_uint32),
-                ("run_epochs", C.c_uint32), ("precision", C.c_int32)]
+                ("run_epochs", C.c_uint32), ("precision", C.c_int32), ("shards", C.c_uint32)]
 
 
 class _Counters(C.Structure):
@@ -146,6 +146,15 @@ SYMBOLS = {
     "f2v_gen_rgg": (_i32, [C.c_uint32, C.c_double, C.c_uint64, C.POINTER(C.POINTER(C.c_uint32)),
                            C.POINTER(C.c_uint64)]),
     "f2v_free": (None, [_vp]),
+    "f2v_shard_layout": (_i32, [C.c_uint32, C.c_uint32, C.c_uint32, _vp, C.POINTER(C.c_uint32)]),
+    "f2v_shard_handle_bytes": (_i32, []),
+    "f2v_shard_init": (_i32, [_vp, C.c_uint32, C.c_uint32]),
+    "f2v_shard_export": (_i32, [_vp, C.c_char_p]),
+    "f2v_shard_attach": (_i32, [_vp, C.c_char_p]),
+    "f2v_partition_shard": (_i32, [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
+                                   C.c_uint32, _u32p]),
+    "f2v_get_rows": (_i32, [_vp, _u32p, C.c_uint32, _f32p]),
+    "f2v_set_rows": (_i32, [_vp, _u32p, C.c_uint32, _f32p]),
 }
 
 
@@ -222,6 +231,7 @@ class TrainConfig:
     monitor_loss: bool = False
     sampler: str = "splitmix"
     precision: str = "fast"  # "fast" (fp32 pair math, fp64 accumulate) or "exact" (fp64)
+    shards: int = 1  # vertex shards G; 1 = the reference's stream
 
     def _c(self, init: int = 0, first_epoch: int = 0, run_epochs: int = 0) -> _TrainConfig:
         if self.lr_decay not in ("constant", "linear_to_zero"):
@@ -236,7 +246,7 @@ class TrainConfig:
                             self.model._c(), self.seed & (2**64 - 1),
                             int(self.lr_decay == "linear_to_zero"), int(self.monitor_loss),
                             SAMPLERS[self.sampler], init, first_epoch, run_epochs,
-                            0 if self.precision == "fast" else 1)
+                            0 if self.precision == "fast" else 1, int(self.shards))
 
 
 @dataclasses.dataclass
@@ -342,6 +352,28 @@ def partition_epoch(n: int, b: int, seed: int, epoch: int) -> np.ndarray:
     return perm
 
 
+def shard_layout(n: int, batch: int, shards: int):
+    """(poff, T): combined step-major layout of G shards (f2v_shard_layout):
+    poff[t*G + g] = first position of shard g's batch t, poff[T*G] = n."""
+    T = C.c_uint32()
+    _check(_lib.f2v_shard_layout(n, batch, shards, None, C.byref(T)))
+    poff = np.zeros(T.value * shards + 1, np.uint32)
+    _check(_lib.f2v_shard_layout(n, batch, shards, poff.ctypes.data_as(_vp), C.byref(T)))
+    return poff, T.value
+
+
+def shard_range(n: int, shards: int, g: int):
+    """rows [lo, hi) of shard g (orc_shard_range)"""
+    return n * g // shards, n * (g + 1) // shards
+
+
+def partition_shard(n: int, b: int, seed: int, epoch: int, shard: int, shards: int) -> np.ndarray:
+    """partition_epoch of one shard's n rows (local ids), keyed (seed,{0x22,epoch[,shard]})."""
+    perm = np.zeros(n, np.uint32)
+    _check(_lib.f2v_partition_shard(n, b, seed, epoch, shard, shards, perm))
+    return perm
+
+
 def negatives(sampler: str, seed: int, epoch: int, batch: int, n: int, s: int, shard: int = 0,
               num_shards: int = 1) -> np.ndarray:
     """The shared negatives of one batch (sampling.cpp:21-25 / Philox)."""
@@ -407,6 +439,32 @@ class Device:
         perm = np.zeros(n, np.uint32)
         self._ck(_lib.f2v_device_partition_epoch(self._h, n, b, seed, epoch, perm))
         return perm
+
+    # ------------------------------------------- multi-GPU shards (dist.py)
+    def shard_init(self, rank: int, world: int):
+        self._ck(_lib.f2v_shard_init(self._h, rank, world))
+
+    def shard_export(self) -> bytes:
+        buf = C.create_string_buffer(_lib.f2v_shard_handle_bytes())
+        self._ck(_lib.f2v_shard_export(self._h, buf))
+        return buf.raw
+
+    def shard_attach(self, handles: list):
+        blob = b"".join(handles)
+        self._ck(_lib.f2v_shard_attach(self._h, blob))
+
+    def get_rows(self, ids) -> np.ndarray:
+        ids = np.ascontiguousarray(ids, np.uint32)
+        out = np.zeros((len(ids), self.d), np.float32)
+        self._ck(_lib.f2v_get_rows(self._h, _nz(ids), len(ids), out.reshape(-1) if len(ids)
+                                   else np.zeros(1, np.float32)))
+        return out
+
+    def set_rows(self, ids, rows: np.ndarray):
+        ids = np.ascontiguousarray(ids, np.uint32)
+        rows = np.ascontiguousarray(rows, np.float32).reshape(-1)
+        self._ck(_lib.f2v_set_rows(self._h, _nz(ids), len(ids), rows if len(rows)
+                                   else np.zeros(1, np.float32)))
 
     def upload_graph(self, g: CsrGraph):
         self._ck(_lib.f2v_upload_graph(self._h, g.num_vertices(), g.row_offsets,

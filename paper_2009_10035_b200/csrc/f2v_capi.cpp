@@ -182,22 +182,30 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
     if (c.d != cfg.dim) fail(F2V_ERANGE, "embedding dim does not match cfg.dim");
   }
   const uint32_t n = c.n;
-  const uint32_t b = std::min(cfg.batch, n);  // trainer.cpp:200
   const uint32_t s = cfg.negatives;
   const ForceParams fp = make_params(cfg.model);
-  const uint64_t nb = (uint64_t(n) + b - 1) / b;
-  c.perm.ensure(sizeof(uint32_t) * n);
+  // G vertex shards: one process per GPU when the
+  // context is attached to peers, else every shard in this process
+  uint32_t G = cfg.shards ? cfg.shards : 1;
+  if (c.world > 1) {
+    if (!cfg.shards) G = c.world;
+    if (G != c.world) fail(F2V_EUSAGE, "cfg.shards must equal the number of attached GPUs");
+  }
+  k_shard_layout(c, cfg.batch, G);  // batch clamped per shard (trainer.cpp:200)
   uint64_t attr = 0, rep = 0;
   for (uint32_t e = cfg.first_epoch; e < end_epoch; ++e) {
     float eta = cfg.lr;
     if (cfg.lr_decay) eta = cfg.lr * (1.0f - float(e) / float(cfg.epochs));
-    // partition_epoch (trainer.cpp:216-217) as a device Fisher-Yates
-    k_device_partition(c, n, cfg.seed, e, c.perm.as<uint32_t>());
-    k_epoch_begin(c, b, s, e, cfg.seed, cfg.sampler);
-    const EpochResult r = k_epoch_run(c, b, s, eta, fp, cfg.monitor_loss != 0);
+    // partition_epoch (trainer.cpp:216-217) as a device Fisher-Yates per shard
+    k_epoch_perm(c, e, cfg.seed);
+    k_epoch_begin(c, s, e, cfg.seed, cfg.sampler);
+    const EpochResult r = k_epoch_run(c, s, eta, fp, cfg.monitor_loss != 0);
     if (r.bad_pos != ~0ull) {
-      const uint64_t jb = r.bad_pos / b;
-      k_epoch_restore(c, b, jb);
+      // the step of the failing position (combined step-major order)
+      const uint64_t T = c.steps;
+      uint64_t jb = 0;
+      while (jb + 1 < T && c.h_poff[(jb + 1) * G] <= r.bad_pos) ++jb;
+      k_epoch_restore(c, jb);
       uint32_t v = 0;
       F2V_CUDA(cudaMemcpy(&v, c.perm.as<uint32_t>() + r.bad_pos, sizeof(v),
                           cudaMemcpyDeviceToHost));
@@ -213,7 +221,6 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
     attr += c.nnz;            // one-hop: every arc once per epoch (trainer.cpp:154-160)
     rep += uint64_t(n) * s;   // b*s per batch (trainer.cpp:161-162)
   }
-  (void)nb;
   if (counters) {
     counters->attractive_evals += attr;
     counters->repulsive_evals += rep;
@@ -268,8 +275,12 @@ void f2v_destroy(f2v_ctx* h) {
         &c.state, &c.negs_all, &c.negwin, &c.items, &c.litems, &c.nE, &c.nL, &c.EP, &c.LP,
         &c.wtot, &c.needs, &c.scan_tmp, &c.epart, &c.eloss, &c.wcnt, &c.wl, &c.lpart, &c.lloss,
         &c.ploss, &c.counters, &c.trace, &c.shufR, &c.shufL, &c.nEng, &c.ecum, &c.epos,
-        &c.eslot, &c.eidx, &c.rcnt})
+        &c.eslot, &c.eidx, &c.rcnt, &c.poff, &c.lperm})
     b->release();
+  for (uint32_t g = 0; g < 8; ++g)  // peers' replicas mapped by f2v_shard_attach
+    for (int i = 0; i < 3; ++i)
+      if (c.peer_base[g][i]) cudaIpcCloseMemHandle(c.peer_base[g][i]);
+  c.ctl.release();
   for (cudaEvent_t e : c.ev_kernel) cudaEventDestroy(e);
   if (c.ev_begin) cudaEventDestroy(c.ev_begin);
   if (c.ev_end) cudaEventDestroy(c.ev_end);
@@ -599,5 +610,123 @@ int32_t f2v_gen_rgg(uint32_t n, double mean_deg, uint64_t seed, uint32_t** pairs
 }
 
 void f2v_free(void* p) { std::free(p); }
+
+// ------------------------------------------ multi-GPU shards (f2v_shard.cu)
+int32_t f2v_shard_layout(uint32_t n, uint32_t batch, uint32_t shards, uint32_t* poff_out,
+                         uint32_t* steps_out) {
+  return guard(nullptr, [&] {
+    std::vector<uint32_t> lo, bs, nb, poff;
+    uint32_t T = 0;
+    shard_layout(n, batch, shards, lo, bs, nb, poff, T);
+    if (steps_out) *steps_out = T;
+    if (poff_out) std::memcpy(poff_out, poff.data(), sizeof(uint32_t) * poff.size());
+  });
+}
+
+int32_t f2v_partition_shard(uint32_t n, uint32_t b, uint64_t seed, uint32_t epoch,
+                            uint32_t shard, uint32_t shards, uint32_t* perm_out) {
+  return guard(nullptr, [&] {
+    if (shards < 1 || shard >= shards) fail(F2V_EUSAGE, "shard out of range");
+    const uint64_t st = shards == 1 ? rng_keyed2(seed, kStreamPartition, epoch)
+                                    : rng_keyed3(seed, kStreamPartition, epoch, shard);
+    partition_epoch(n, b, st, perm_out);
+  });
+}
+
+static void rows_io(Ctx& c, const uint32_t* ids, uint32_t b, float* host, bool to_z) {
+  need_embedding(c);
+  F2V_CUDA(cudaSetDevice(c.device));
+  for (uint32_t i = 0; i < b; ++i)
+    if (ids[i] >= c.n) fail(F2V_ERANGE, "vertex id out of range");
+  c.ids.ensure(sizeof(uint32_t) * std::max<uint32_t>(b, 1));
+  c.scratch.ensure(sizeof(float) * std::max<size_t>(size_t(b) * c.d, 8));
+  const size_t bytes = sizeof(float) * size_t(b) * c.d;
+  if (b)
+    F2V_CUDA(cudaMemcpyAsync(c.ids.p, ids, sizeof(uint32_t) * b, cudaMemcpyHostToDevice,
+                             c.stream));
+  if (to_z && b)
+    F2V_CUDA(cudaMemcpyAsync(c.scratch.p, host, bytes, cudaMemcpyHostToDevice, c.stream));
+  k_rows(c, b, c.scratch.as<float>(), to_z);
+  if (!to_z && b)
+    F2V_CUDA(cudaMemcpyAsync(host, c.scratch.p, bytes, cudaMemcpyDeviceToHost, c.stream));
+  F2V_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+int32_t f2v_get_rows(f2v_ctx* h, const uint32_t* ids, uint32_t b, float* rows_out) {
+  return guard(&h->c, [&] { rows_io(h->c, ids, b, rows_out, false); });
+}
+
+int32_t f2v_set_rows(f2v_ctx* h, const uint32_t* ids, uint32_t b, const float* rows) {
+  return guard(&h->c, [&] { rows_io(h->c, ids, b, const_cast<float*>(rows), true); });
+}
+
+int32_t f2v_shard_handle_bytes(void) { return int32_t(3 * sizeof(cudaIpcMemHandle_t)); }
+
+int32_t f2v_shard_init(f2v_ctx* h, uint32_t rank, uint32_t world) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    F2V_CUDA(cudaSetDevice(c.device));
+    if (world < 1 || world > 8) fail(F2V_EUSAGE, "world must be in [1, 8]");
+    if (rank >= world) fail(F2V_EUSAGE, "rank out of range");
+    if (!c.rowptr.p) fail(F2V_EUSAGE, "upload the graph before f2v_shard_init");
+    if (!c.z[c.cur].p || !c.d) fail(F2V_EUSAGE, "set the embedding before f2v_shard_init");
+    if (c.n < world) fail(F2V_EUSAGE, "fewer vertices than shards");
+    if (c.rank >= 0) fail(F2V_EUSAGE, "context already sharded");
+    // both replica buffers exist from now on and never move (peers map them)
+    const size_t zb = sizeof(float) * size_t(c.n) * c.d;
+    c.z[0].ensure(zb);
+    c.z[1].ensure(zb);
+    c.ctl.ensure(shard_ctl_bytes());
+    F2V_CUDA(cudaMemsetAsync(c.ctl.p, 0, shard_ctl_bytes(), c.stream));
+    F2V_CUDA(cudaStreamSynchronize(c.stream));
+    c.rank = int32_t(rank);
+    c.world = world;
+    c.barriers = 0;
+    c.layout_key[2] = 0;  // re-plan the layout with the ownership
+  });
+}
+
+int32_t f2v_shard_export(f2v_ctx* h, uint8_t* out) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    if (c.rank < 0) fail(F2V_EUSAGE, "f2v_shard_init first");
+    F2V_CUDA(cudaSetDevice(c.device));
+    void* bufs[3] = {c.z[0].p, c.z[1].p, c.ctl.p};
+    for (int i = 0; i < 3; ++i) {
+      cudaIpcMemHandle_t hd;
+      F2V_CUDA(cudaIpcGetMemHandle(&hd, bufs[i]));
+      std::memcpy(out + i * sizeof(hd), &hd, sizeof(hd));
+    }
+  });
+}
+
+int32_t f2v_shard_attach(f2v_ctx* h, const uint8_t* all) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    if (c.rank < 0) fail(F2V_EUSAGE, "f2v_shard_init first");
+    if (c.shard_ready) fail(F2V_EUSAGE, "context already attached");
+    F2V_CUDA(cudaSetDevice(c.device));
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    for (uint32_t g = 0; g < c.world; ++g) {
+      if (int32_t(g) == c.rank) {
+        c.peer_z[g][0] = c.z[0].as<float>();
+        c.peer_z[g][1] = c.z[1].as<float>();
+        c.peer_ctl[g] = c.ctl.p;
+        continue;
+      }
+      for (int i = 0; i < 3; ++i) {
+        cudaIpcMemHandle_t hd;
+        std::memcpy(&hd, all + (size_t(g) * 3 + i) * hb, hb);
+        void* p = nullptr;
+        F2V_CUDA(cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess));
+        c.peer_base[g][i] = p;
+      }
+      c.peer_z[g][0] = static_cast<float*>(c.peer_base[g][0]);
+      c.peer_z[g][1] = static_cast<float*>(c.peer_base[g][1]);
+      c.peer_ctl[g] = c.peer_base[g][2];
+    }
+    c.shard_ready = true;
+  });
+}
 
 }  // extern "C"

@@ -45,18 +45,35 @@ namespace {
 using namespace dev;
 
 // ------------------------------------------------------ per-epoch prep
-__global__ void state_kernel(const uint32_t* __restrict__ perm, uint32_t* __restrict__ state,
-                             uint32_t n, uint32_t b, const uint32_t* __restrict__ cbase,
-                             uint32_t* __restrict__ nE, uint32_t* __restrict__ wtot) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p > n) return;
-  if (p == n) {
-    nE[n] = 0;
+// Shard geometry for the device (G <= kMaxShards).
+struct ShardGeo {
+  uint32_t n, G, rank_lo, rank_hi;  // owned rows [rank_lo, rank_hi) (all: [0, n))
+  uint32_t lo[ep::kMaxShards + 1], bs[ep::kMaxShards], nb[ep::kMaxShards];
+};
+
+// Combined step-major order: local position i of shard g (its Fisher-Yates
+// perm in lperm[lo_g + i]) lands at poff[t G + g] + i % bs_g with t = i / bs_g
+// (orc_train: step t = every shard's t-th local batch).  Writes the combined
+// perm, state[u] = t << 1, and the E-chunk count of owned positions.
+__global__ void scatter_kernel(const uint32_t* __restrict__ lperm, const uint32_t* __restrict__ poff,
+                               ShardGeo geo, const uint32_t* __restrict__ cbase,
+                               uint32_t* __restrict__ perm, uint32_t* __restrict__ state,
+                               uint32_t* __restrict__ nE, uint32_t* __restrict__ wtot) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x > geo.n) return;
+  if (x == geo.n) {
+    nE[geo.n] = 0;
     return;
   }
-  const uint32_t u = perm[p];
-  state[u] = (p / b) << 1;
-  nE[p] = cbase[u + 1] - cbase[u];
+  const uint32_t g = ep::shard_of(x, geo.n, geo.G);
+  const uint32_t i = x - geo.lo[g];
+  const uint32_t u = geo.lo[g] + lperm[x];
+  const uint32_t t = i / geo.bs[g];
+  const uint32_t pos = poff[t * geo.G + g] + i % geo.bs[g];
+  perm[pos] = u;
+  state[u] = t << 1;
+  const bool own = u >= geo.rank_lo && u < geo.rank_hi;
+  nE[pos] = own ? cbase[u + 1] - cbase[u] : 0u;
   wtot[u] = 0;
 }
 
@@ -82,10 +99,12 @@ __global__ void src_kernel(const uint64_t* __restrict__ rowptr, uint32_t* __rest
   for (uint64_t e = rowptr[u] + lane; e < rowptr[u + 1]; e += 32) src[e] = u;
 }
 
-__global__ void needs_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint32_t b,
+__global__ void needs_kernel(const uint32_t* __restrict__ perm, ShardGeo geo,
+                             const uint32_t* __restrict__ state,
                              const uint32_t* __restrict__ wtot, const uint32_t* __restrict__ negwin,
                              const uint32_t* __restrict__ lbase, uint32_t* __restrict__ needs,
                              uint32_t* __restrict__ nL, uint32_t* __restrict__ nEng, int nodep) {
+  const uint32_t n = geo.n;
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > n) return;
   if (p == n) {
@@ -94,11 +113,13 @@ __global__ void needs_kernel(const uint32_t* __restrict__ perm, uint32_t n, uint
     return;
   }
   const uint32_t u = perm[p];
-  const uint32_t nw = negwin[p / b];
+  const uint32_t j = state[u] >> 1;
+  const uint32_t nw = negwin[geo.G == 1 ? j : j * geo.G + ep::shard_of(u, n, geo.G)];
   uint32_t nd = ((wtot[u] | nw) & 1u) && !nodep ? 1u : 0u;
   if (nd && (wtot[u] & 2u) && lbase[u + 1] - lbase[u] == 1) nd |= 2u;  // the chain engine's
   needs[u] = nd;
-  nL[p] = nd ? lbase[u + 1] - lbase[u] : 0u;
+  const bool own = u >= geo.rank_lo && u < geo.rank_hi;
+  nL[p] = nd && own ? lbase[u + 1] - lbase[u] : 0u;
   nEng[p] = (nd & 2u) ? 1u : 0u;
 }
 
@@ -126,21 +147,28 @@ __global__ void engine_emit_kernel(const uint32_t* __restrict__ ecum,
   eidx[u] = i;
 }
 
+// negatives of every (step, shard) set q = t G + g, and whether any of them is
+// a window row of step t (then its vertices need an L item)
 __global__ void negs_kernel(uint32_t* __restrict__ out, uint32_t* __restrict__ negwin,
-                            const uint32_t* __restrict__ state, uint64_t nb, uint32_t s,
-                            uint32_t n, uint64_t seed, uint32_t epoch, int sampler, uint32_t W,
+                            const uint32_t* __restrict__ state, ShardGeo geo, uint64_t nsets,
+                            uint32_t s, uint64_t seed, uint32_t epoch, int sampler, uint32_t W,
                             uint32_t Re) {
-  const uint64_t j = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= nb) return;
+  const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= nsets) return;
+  const uint32_t G = geo.G, g = uint32_t(q % G);
+  const uint64_t j = q / G;
   uint32_t win = 0;
-  for (uint32_t k = 0; k < s; ++k) {
-    const uint32_t w = sampler == F2V_SAMPLER_PHILOX ? philox_negative(seed, epoch, j, 0, k, n)
-                                                     : splitmix_negative(seed, epoch, j, 0, 1, k, n);
-    out[j * s + k] = w;
-    const uint32_t bw = state[w] >> 1;
-    if (bw < j && uint64_t(bw) + W >= j) win |= uint64_t(bw) + Re >= j ? 3u : 1u;
+  if (j < geo.nb[g]) {
+    for (uint32_t k = 0; k < s; ++k) {
+      const uint32_t w = sampler == F2V_SAMPLER_PHILOX
+                             ? philox_negative(seed, epoch, j, g, k, geo.n)
+                             : splitmix_negative(seed, epoch, j, g, G, k, geo.n);
+      out[q * s + k] = w;
+      const uint32_t bw = state[w] >> 1;
+      if (bw < j && uint64_t(bw) + W >= j) win |= uint64_t(bw) + Re >= j ? 3u : 1u;
+    }
   }
-  negwin[j] = win;
+  negwin[q] = win;
 }
 
 // Znew := the sentinel NaN everywhere (rows become readable once stored).
@@ -156,14 +184,19 @@ __global__ void sentinel_tail_kernel(float* __restrict__ z, uint64_t from, uint6
   if (i < to) z[i] = __uint_as_float(kSentinel);
 }
 
-// On a NumericalError at batch jb: rows of batches >= jb go back to Zold so
-// Znew is the state after the last complete batch (trainer.cpp:149-152).
+// On a NumericalError at step jb: rows of steps >= jb go back to Zold so
+// Znew is the state after the last complete step (trainer.cpp:149-152).
 __global__ void restore_kernel(const uint32_t* __restrict__ state, const float* __restrict__ zold,
                                float* __restrict__ znew, uint32_t n, uint32_t d, uint64_t jb) {
   const uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (t >= uint64_t(n) * d) return;
   const uint32_t v = uint32_t(t / d);
   if ((state[v] >> 1) >= jb) znew[t] = zold[t];
+}
+
+__global__ void zero_kernel(double* __restrict__ v, uint64_t m) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < m) v[i] = 0.0;
 }
 
 uint32_t env_u32(const char* name, uint32_t dflt) {
@@ -240,24 +273,110 @@ void k_prepare_graph(Ctx& c) {
   F2V_CUDA(cudaStreamSynchronize(c.stream));
 }
 
-// Per-epoch preparation: perm (already in c.perm) -> state, the negatives of
-// every batch + window flags, the window pre-scan, the two ordered item lists.
-void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed, int sampler) {
+// Host: shard g of G owns rows [n g / G, n (g+1) / G) (orc_shard_range) with
+// batch bs_g = min(batch, size_g) (trainer.cpp:200) and nb_g local batches.
+// Step t = the t-th local batch of every shard, laid out shard by shard:
+// poff[t G + g] = combined position of shard g's batch t; poff[T G] = n.
+void shard_layout(uint32_t n, uint32_t batch, uint32_t G, std::vector<uint32_t>& lo,
+                  std::vector<uint32_t>& bs, std::vector<uint32_t>& nb,
+                  std::vector<uint32_t>& poff, uint32_t& T) {
+  if (G < 1 || G > uint32_t(ep::kMaxShards)) fail(F2V_EUSAGE, "shards must be in [1, 8]");
+  if (n < G) fail(F2V_EUSAGE, "fewer vertices than shards");
+  if (batch < 1) fail(F2V_EUSAGE, "batch must be >= 1");
+  lo.assign(G + 1, 0);
+  bs.assign(G, 0);
+  nb.assign(G, 0);
+  T = 0;
+  for (uint32_t g = 0; g <= G; ++g) lo[g] = uint32_t(uint64_t(n) * g / G);
+  for (uint32_t g = 0; g < G; ++g) {
+    const uint32_t sz = lo[g + 1] - lo[g];
+    bs[g] = std::min(batch, sz);
+    nb[g] = (sz + bs[g] - 1) / bs[g];
+    T = std::max(T, nb[g]);
+  }
+  poff.assign(size_t(T) * G + 1, 0);
+  uint64_t pos = 0;
+  for (uint32_t t = 0; t < T; ++t)
+    for (uint32_t g = 0; g < G; ++g) {
+      poff[size_t(t) * G + g] = uint32_t(pos);
+      if (t < nb[g]) pos += std::min<uint64_t>(bs[g], lo[g + 1] - lo[g] - uint64_t(t) * bs[g]);
+    }
+  poff[size_t(T) * G] = uint32_t(pos);
+}
+
+void k_shard_layout(Ctx& c, uint32_t batch, uint32_t G) {
+  if (c.layout_key[0] == c.n && c.layout_key[1] == batch && c.layout_key[2] == G && c.steps)
+    return;
+  shard_layout(c.n, batch, G, c.sh_lo, c.sh_bs, c.sh_nb, c.h_poff, c.steps);
+  c.poff.ensure(sizeof(uint32_t) * c.h_poff.size());
+  F2V_CUDA(cudaMemcpyAsync(c.poff.p, c.h_poff.data(), sizeof(uint32_t) * c.h_poff.size(),
+                           cudaMemcpyHostToDevice, c.stream));
+  F2V_CUDA(cudaStreamSynchronize(c.stream));
+  c.shards = G;
+  c.layout_key[0] = c.n;
+  c.layout_key[1] = batch;
+  c.layout_key[2] = G;
+}
+
+static ShardGeo make_geo(const Ctx& c) {
+  ShardGeo g{};
+  g.n = c.n;
+  g.G = c.shards;
+  for (uint32_t i = 0; i <= c.shards; ++i) g.lo[i] = c.sh_lo[i];
+  for (uint32_t i = 0; i < c.shards; ++i) {
+    g.bs[i] = c.sh_bs[i];
+    g.nb[i] = c.sh_nb[i];
+  }
+  if (c.rank >= 0) {
+    g.rank_lo = c.sh_lo[c.rank];
+    g.rank_hi = c.sh_lo[c.rank + 1];
+  } else {
+    g.rank_lo = 0;
+    g.rank_hi = c.n;
+  }
+  return g;
+}
+
+// partition_epoch of every shard (sampling.cpp:7-19; shard g > 0 of a sharded
+// run keys its stream (seed, {0x22, epoch, g})) on the device, scattered into
+// the combined step-major order with each vertex's step.
+void k_epoch_perm(Ctx& c, uint32_t epoch, uint64_t seed) {
+  const uint32_t n = c.n, G = c.shards;
+  c.perm.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  c.lperm.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  c.state.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  c.nE.ensure(sizeof(uint32_t) * (n + 1));
+  c.wtot.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
+  for (uint32_t g = 0; g < G; ++g) {
+    const uint64_t s0 = G == 1 ? rng_keyed2(seed, kStreamPartition, epoch)
+                               : rng_keyed3(seed, kStreamPartition, epoch, g);
+    k_device_partition_keyed(c, c.sh_lo[g + 1] - c.sh_lo[g], s0,
+                             c.lperm.as<uint32_t>() + c.sh_lo[g]);
+  }
+  scatter_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
+      c.lperm.as<uint32_t>(), c.poff.as<uint32_t>(), make_geo(c), c.cbase.as<uint32_t>(),
+      c.perm.as<uint32_t>(), c.state.as<uint32_t>(), c.nE.as<uint32_t>(),
+      c.wtot.as<uint32_t>());
+  F2V_LAUNCHED(c.stream, "scatter_kernel");
+  ++c.launches;
+}
+
+// Per-epoch preparation after k_epoch_perm: the negatives of every (step,
+// shard) set + window flags, the window pre-scan, the two ordered item lists
+// (only this process's rows when the shards run on several GPUs).
+void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sampler) {
   const uint32_t n = c.n;
-  const uint32_t nb = uint32_t((uint64_t(n) + b - 1) / b);
+  const uint64_t nsets = uint64_t(c.steps) * c.shards;
   if (c.prepared_chunk != c.tune.chunk || c.prepared_lgroup != c.tune.lgroup)
     k_prepare_graph(c);
-  c.state.ensure(sizeof(uint32_t) * n);
-  c.nE.ensure(sizeof(uint32_t) * (n + 1));
   c.nL.ensure(sizeof(uint32_t) * (n + 1));
   c.EP.ensure(sizeof(uint32_t) * (n + 1));
   c.LP.ensure(sizeof(uint32_t) * (n + 1));
-  c.wtot.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
   c.needs.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
   c.items.ensure(sizeof(uint2) * std::max<uint64_t>(c.chunks, 1));
   c.litems.ensure(sizeof(uint2) * std::max<uint64_t>(c.lgroups, 1));
-  c.negs_all.ensure(sizeof(uint32_t) * std::max<uint64_t>(uint64_t(nb) * s, 1));
-  c.negwin.ensure(sizeof(uint32_t) * std::max<uint32_t>(nb, 1));
+  c.negs_all.ensure(sizeof(uint32_t) * std::max<uint64_t>(nsets * s, 1));
+  c.negwin.ensure(sizeof(uint32_t) * std::max<uint64_t>(nsets, 1));
   c.epart.ensure(sizeof(double) * std::max<uint64_t>(c.chunks * c.d, 1));
   c.eloss.ensure(sizeof(double) * std::max<uint64_t>(c.chunks, 1));
   c.wcnt.ensure(sizeof(uint32_t) * std::max<uint64_t>(c.chunks, 1));
@@ -274,7 +393,7 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
                          ((size_t(c.d) * 12 + ep::kRefStride * 4 + 15) / 16 * 16);
     const size_t budget = 210u * 1024u > stage ? 210u * 1024u - stage : 0;
     c.eff_maxe = Re ? uint32_t(std::min<size_t>(64, budget / (size_t(Re + 1) * c.d * 4))) : 0u;
-    if (Re && (!c.tune.fast || c.eff_maxe < 4 || n >= kIdMask ||
+    if (Re && (!c.tune.fast || c.eff_maxe < 4 || n >= kIdMask || c.shards != 1 ||
                (c.d != 64 && c.d != 128 && c.d != 256)))
       Re = 0;
     c.eff_re = Re;
@@ -285,14 +404,10 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
   c.eslot.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
   c.eidx.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
   c.rcnt.ensure(sizeof(uint32_t) * ep::kRefStride * std::max<uint32_t>(n, 1));
-  state_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(c.perm.as<uint32_t>(),
-                                                         c.state.as<uint32_t>(), n, b,
-                                                         c.cbase.as<uint32_t>(),
-                                                         c.nE.as<uint32_t>(), c.wtot.as<uint32_t>());
-  F2V_LAUNCHED(c.stream, "state_kernel");
-  negs_kernel<<<(nb + 255) / 256, 256, 0, c.stream>>>(
-      c.negs_all.as<uint32_t>(), c.negwin.as<uint32_t>(), c.state.as<uint32_t>(), nb, s, n, seed,
-      epoch, sampler, W, Re);
+  const ShardGeo geo = make_geo(c);
+  negs_kernel<<<uint32_t((nsets + 255) / 256), 256, 0, c.stream>>>(
+      c.negs_all.as<uint32_t>(), c.negwin.as<uint32_t>(), c.state.as<uint32_t>(), geo, nsets, s,
+      seed, epoch, sampler, W, Re);
   F2V_LAUNCHED(c.stream, "negs_kernel");
   if (c.nnz)
     window_scan_kernel<<<uint32_t((c.nnz + 255) / 256), 256, 0, c.stream>>>(
@@ -300,9 +415,9 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
         c.wtot.as<uint32_t>(), c.nnz, W, Re);
   F2V_LAUNCHED(c.stream, "window_scan_kernel");
   needs_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
-      c.perm.as<uint32_t>(), n, b, c.wtot.as<uint32_t>(), c.negwin.as<uint32_t>(),
-      c.lbase.as<uint32_t>(), c.needs.as<uint32_t>(), c.nL.as<uint32_t>(), c.nEng.as<uint32_t>(),
-      std::getenv("F2V_DEBUG_NODEP") ? 1 : 0);
+      c.perm.as<uint32_t>(), geo, c.state.as<uint32_t>(), c.wtot.as<uint32_t>(),
+      c.negwin.as<uint32_t>(), c.lbase.as<uint32_t>(), c.needs.as<uint32_t>(),
+      c.nL.as<uint32_t>(), c.nEng.as<uint32_t>(), std::getenv("F2V_DEBUG_NODEP") ? 1 : 0);
   F2V_LAUNCHED(c.stream, "needs_kernel");
   size_t tmp = 0;
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.nE.as<uint32_t>(), c.EP.as<uint32_t>(),
@@ -324,22 +439,29 @@ void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed
     engine_emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(
         c.ecum.as<uint32_t>(), c.nEng.as<uint32_t>(), c.perm.as<uint32_t>(),
         c.cbase.as<uint32_t>(), c.epos.as<uint4>(), c.eslot.as<uint32_t>(),
-        c.eidx.as<uint32_t>(), n, b);
+        c.eidx.as<uint32_t>(), n, c.sh_bs[0]);
     F2V_LAUNCHED(c.stream, "engine_emit_kernel");
   }
-  // number of L items (device value, read back asynchronously with the run)
+  // numbers of E and L items (device values, read back asynchronously with the run)
   F2V_CUDA(cudaMemcpyAsync(c.counters.as<uint32_t>() + 8, c.LP.as<uint32_t>() + n,
                            sizeof(uint32_t), cudaMemcpyDeviceToDevice, c.stream));
-  c.launches += 9;
+  F2V_CUDA(cudaMemcpyAsync(c.counters.as<uint32_t>() + 9, c.EP.as<uint32_t>() + n,
+                           sizeof(uint32_t), cudaMemcpyDeviceToDevice, c.stream));
+  c.launches += 7;
 }
 
-EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForceParams& fp,
-                        bool monitor) {
+EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bool monitor) {
   const int nxt = 1 - c.cur;
+  const bool multi = c.shard_ready;  // attached (also world 1: exercises the barrier path)
   c.z[nxt].ensure(sizeof(float) * size_t(c.n) * c.d);
-  uint32_t* ctr = c.counters.as<uint32_t>();  // [0..1] claims, [2..3] bad, [4..5] loss, [8] nL
+  uint32_t* ctr = c.counters.as<uint32_t>();  // [0..1] claims, [2..3] bad, [4..5] loss, [8] nL, [9] nE
   F2V_CUDA(cudaMemsetAsync(ctr, 0, 8, c.stream));
   F2V_CUDA(cudaMemsetAsync(ctr + 2, 0xff, 8, c.stream));
+  if (monitor && multi) {  // only this process's positions are finalised here
+    zero_kernel<<<(c.n + 255) / 256, 256, 0, c.stream>>>(c.ploss.as<double>(), c.n);
+    F2V_LAUNCHED(c.stream, "zero_kernel");
+    ++c.launches;
+  }
   {  // Znew := sentinel (cudaMalloc'd buffers are 256-byte aligned)
     const uint64_t total = uint64_t(c.n) * c.d, n16 = total / 4;
     sentinel_kernel<<<uint32_t(std::min<uint64_t>((n16 + 255) / 256, 4u * c.num_sms * 8)), 256, 0,
@@ -349,6 +471,8 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
       sentinel_tail_kernel<<<1, 4, 0, c.stream>>>(c.z[nxt].as<float>(), n16 * 4, total);
     c.launches += 1;
   }
+  // every replica holds the sentinel before any GPU stores a row into it
+  if (multi) k_shard_barrier(c);
   ep::EpochArgs a;
   a.rowptr = c.rowptr.as<uint64_t>();
   a.col = c.col.as<uint32_t>();
@@ -361,6 +485,7 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.eitems = c.items.as<uint2>();
   a.litems = c.litems.as<uint2>();
   a.n_eitems = uint32_t(c.chunks);
+  a.n_eitems_dev = ctr + 9;
   a.n_litems = ctr + 8;
   a.next = ctr;
   a.cbase = c.cbase.as<uint32_t>();
@@ -380,13 +505,19 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.bad = reinterpret_cast<unsigned long long*>(ctr + 2);
   a.n = c.n;
   a.d = c.d;
-  a.b = b;
+  a.b = c.sh_bs[0];
   a.s = s;
   a.C = c.tune.chunk;
   a.G = c.tune.lgroup;
   a.W = c.tune.window;
   a.R = c.tune.recent;
   a.lwarps = c.tune.lwarps;
+  a.shards = c.shards;
+  a.npeers = 0;
+  for (int g = 0; g < ep::kMaxShards; ++g) a.peer_znew[g] = nullptr;
+  if (multi)
+    for (uint32_t g = 0; g < c.world; ++g)
+      if (int32_t(g) != c.rank) a.peer_znew[a.npeers++] = c.peer_z[g][nxt];
   a.rl = c.rcnt.as<uint32_t>();
   a.erec = c.epos.as<uint4>();
   a.ecum = c.ecum.as<uint32_t>();
@@ -404,7 +535,7 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   a.ltrace = nullptr;
   a.etrace = nullptr;
   if (std::getenv("F2V_TRACE")) {
-    const uint32_t nbt = (c.n + b - 1) / b;
+    const uint32_t nbt = c.steps;
     c.trace.ensure(sizeof(unsigned long long) * (5ull * std::max<uint32_t>(c.n, 1) + 3ull * nbt + 2));
     a.trace = c.trace.as<unsigned long long>();
     a.ltrace = a.trace + c.n;
@@ -436,15 +567,22 @@ EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForcePa
   c.last_litems = uint32_t(host[4]);
   EpochResult r{host[1], 0.0};
   if (monitor) std::memcpy(&r.loss, &host[2], sizeof(double));
+  if (multi) {
+    // every GPU's first failure and loss partial into every replica's control
+    // block; after the barrier all ranks hold the same global values (the
+    // loss summed in rank order: identical on every rank)
+    k_shard_publish(c, r.bad_pos, r.loss);
+    k_shard_barrier(c);
+    k_shard_collect(c, r.bad_pos, r.loss);
+  }
   c.cur = nxt;  // Znew becomes the current embedding
   return r;
 }
 
-void k_epoch_restore(Ctx& c, uint32_t b, uint64_t bad_batch) {
-  (void)b;
+void k_epoch_restore(Ctx& c, uint64_t bad_step) {
   const uint64_t total = uint64_t(c.n) * c.d;
   restore_kernel<<<uint32_t((total + 255) / 256), 256, 0, c.stream>>>(
-      c.state.as<uint32_t>(), c.z[1 - c.cur].as<float>(), c.zcur(), c.n, c.d, bad_batch);
+      c.state.as<uint32_t>(), c.z[1 - c.cur].as<float>(), c.zcur(), c.n, c.d, bad_step);
   F2V_LAUNCHED(c.stream, "restore_kernel");
   ++c.launches;
   F2V_CUDA(cudaStreamSynchronize(c.stream));

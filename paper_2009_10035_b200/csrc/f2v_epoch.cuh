@@ -27,6 +27,7 @@ constexpr int kQ = 64;          // per-warp compaction queue (entries)
 constexpr int kRq = 64;         // per-warp parking lot for the most recent window arcs
 constexpr int kRefs = 32;       // engine: ring refs per vertex (+1 count word); more go global
 constexpr int kRefStride = 36;  // words per vertex ref area (16-byte multiple for cp.async)
+constexpr int kMaxShards = 8;   // vertex shards (GPUs) of one run
 
 struct EpochArgs {
   const uint64_t* rowptr;
@@ -39,7 +40,8 @@ struct EpochArgs {
   const uint32_t* negwin;
   const uint2* eitems;
   const uint2* litems;
-  uint32_t n_eitems;
+  uint32_t n_eitems;                 // host upper bound (grid sizing)
+  const uint32_t* n_eitems_dev;      // device count (written by the prep)
   const uint32_t* n_litems;  // device count (written by the prep)
   uint32_t* next;  // [0] E claims, [1] L claims
   const uint32_t* cbase;
@@ -59,6 +61,11 @@ struct EpochArgs {
   unsigned long long* bad;
   uint32_t n, d, b, s;
   uint32_t C, G, W, R, lwarps;
+  // vertex-partitioned shards: step j of a vertex = state >> 1,
+  // its negatives = set j * shards + shard(u); finalised rows are also stored
+  // into the peers' Znew replicas (NVLink P2P) when npeers > 0
+  uint32_t shards, npeers;
+  float* peer_znew[kMaxShards];
   uint32_t Re;              // chain engine: arcs of age <= Re to ring rows are its (0 = off)
   uint32_t* rl;             // engine: per engine vertex [count, ring refs...] (kRefs words)
   const uint4* erec;        // engine: per engine index {vertex, cbase, position, 0}
@@ -99,6 +106,15 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
+// shard g owns rows [floor(n g / G), floor(n (g+1) / G)) (orc_shard_range)
+__device__ __forceinline__ uint32_t shard_of(uint32_t u, uint32_t n, uint32_t G) {
+  return G == 1 ? 0u : uint32_t((uint64_t(u + 1) * G - 1) / n);
+}
+// index of the negative set of a vertex of step j: one set per (step, shard)
+__device__ __forceinline__ uint32_t neg_set(const EpochArgs& a, uint32_t u, uint32_t j) {
+  return a.shards == 1 ? j : j * a.shards + shard_of(u, a.n, a.shards);
+}
+
 // Per-warp FIFO of packed row ids (bit 31 = Znew) in shared memory; rows
 // are accumulated 32 at a time in push order (= the deterministic pair order).
 template <int KIND, int K, bool VEC, bool MON, bool FAST, bool ATT>
@@ -136,14 +152,14 @@ struct RowQueue {
 
 // The shared negatives of batch j, in sample order (sampling.cpp:59).
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
-__device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, int lane,
+__device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, uint32_t q, int lane,
                                              const float (&zu)[K], double (&acc)[K],
                                              double& lsum) {
   for (uint32_t k0 = 0; k0 < a.s; k0 += 32) {
     const int cnt = int(umin32(32, a.s - k0));
     uint32_t pk = 0;
     if (lane < cnt) {
-      const uint32_t w = a.negs[size_t(j) * a.s + k0 + lane];
+      const uint32_t w = a.negs[size_t(q) * a.s + k0 + lane];
       const uint32_t st = ld_relaxed(a.state + w);
       if ((st >> 1) < j && !a.nodep) {
         pk = w | kNewBit;  // Znew row: the row loads poll its sentinel
@@ -154,6 +170,14 @@ __device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, int
     Rows<KIND, K, VEC, MON, FAST>::template run<false>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew,
                                                        zu, acc, lsum);
   }
+}
+
+// the row into every peer GPU's Znew replica (multi-GPU shards), out of line
+template <int K, bool VEC>
+__device__ __noinline__ void store_peers(const EpochArgs& a, uint32_t u, int lane,
+                                         const float (&nz)[K]) {
+  for (uint32_t g = 0; g < a.npeers; ++g)
+    Lay<K, VEC>::store(a.peer_znew[g] + size_t(u) * a.d, lane, a.d, nz);
 }
 
 // g = float(acc) (trainer.cpp:140-145); z_u -= eta*g in fp32 (trainer.cpp:173);
@@ -174,6 +198,7 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_
   }
   if (ring_row) L::store_smem(ring_row, lane, a.d, nz);    // the chain engine's own copy
   L::store(a.znew + size_t(u) * a.d, lane, a.d, nz);  // publishes the row (sentinel-free)
+  if (a.npeers) store_peers<K, VEC>(a, u, lane, nz);  // the peers' replicas, over NVLink
   const bool any_bad = __any_sync(kFull, bad);
   if (MON) {
     const double tot = warp_sum_d(lsum);
@@ -191,7 +216,7 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
   DCHECK(p < a.n, "E p=%u n=%u", p, a.n);
   const uint32_t u = a.perm[p];
   DCHECK(u < a.n, "E u=%u", u);
-  const uint32_t j = p / a.b;
+  const uint32_t j = __ldg(a.state + u) >> 1;
   const uint64_t r0 = a.rowptr[u], r1 = a.rowptr[u + 1];
   const uint32_t cb = a.cbase[u];
   const uint32_t nch = a.cbase[u + 1] - cb;
@@ -239,7 +264,7 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
   const bool needs = a.needs[u] != 0;
   if (nch == 1) {
     if (!needs) {
-      do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+      do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
       finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
     } else {
       L::store_acc(a.epart + size_t(cs) * a.d, lane, a.d, acc);
@@ -278,7 +303,7 @@ __device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint3
   }
   if (lane == 0) a.ecnt[u] = 0;
   if (!needs) {
-    do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+    do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
     finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
   } else {
     L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);  // the E total
@@ -396,7 +421,7 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   DCHECK(p < a.n, "L p=%u", p);
   const uint32_t u = a.perm[p];
   DCHECK(u < a.n, "L u=%u", u);
-  const uint32_t j = p / a.b;
+  const uint32_t j = __ldg(a.state + u) >> 1;
   const uint32_t cb = a.cbase[u];
   const uint32_t nch = a.cbase[u + 1] - cb;
   const uint32_t nchL = a.lbase[u + 1] - a.lbase[u];
@@ -425,7 +450,7 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     if (eng) {  // E total + window arcs except ring refs + negatives -> pre-final P(u)
       window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
                                               lsum, true);
-      do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+      do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
       L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
       const double ls = MON ? warp_sum_d(lsum) : 0.0;
       if (lane == 0) {
@@ -440,7 +465,7 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     }
     // E total + old window arcs + negatives + recent arcs
     window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
-    do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+    do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
     if (lt && lane == 0) lt[2] = globaltimer();
     recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
     if (lt && lane == 0) lt[3] = globaltimer();
@@ -473,7 +498,7 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     L::add_acc(a.lpart + size_t(lp + qq) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __dadd_rn(lsum, __ldcg(a.lloss + lp + qq));
   }
-  do_negatives<KIND, K, VEC, MON, FAST>(a, j, lane, zu, acc, lsum);
+  do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
   if (lane == 0) a.lcnt[u] = 0;
   finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
   if (lane == 0) a.vflag[u] = 0;
@@ -489,7 +514,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) epoch_kernel(EpochArgs a) {
   uint32_t* rbuf = rs[w];
   const bool lrole = w >= kWarps - int(a.lwarps);
   uint32_t* counter = a.next + (lrole ? 1 : 0);
-  const uint32_t total = lrole ? *a.n_litems : a.n_eitems;
+  const uint32_t total = lrole ? *a.n_litems : *a.n_eitems_dev;
   const uint2* items = lrole ? a.litems : a.eitems;
   uint32_t it = 0;
   if (lane == 0) it = atomicAdd(counter, 1u);

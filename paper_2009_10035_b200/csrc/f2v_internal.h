@@ -89,6 +89,22 @@ struct Ctx {
   cudaStream_t stream2 = nullptr;                 // the chain engine runs here
   cudaEvent_t ev_prep = nullptr, ev_engine = nullptr;
   uint32_t eff_re = 0, eff_maxe = 0;              // engine window / ring rows this epoch
+  // vertex shards: G shards, step-major combined order
+  uint32_t shards = 1;        // G of the current run
+  int32_t rank = -1;          // this process's shard; -1 = one process runs every shard
+  uint32_t world = 1;         // processes (GPUs) sharing the run through peer replicas
+  DeviceBuf poff, lperm;      // combined start of (step, shard) batches; per-shard perms
+  std::vector<uint32_t> h_poff;
+  uint32_t steps = 0;         // T = max over shards of the local batch count
+  uint64_t layout_key[3] = {0, 0, 0};
+  std::vector<uint32_t> sh_lo, sh_bs, sh_nb;  // per shard: first row, batch, batches
+  // multi-process: IPC-shared control block + the peers' replicas (f2v_shard.cu)
+  DeviceBuf ctl;
+  bool shard_ready = false;
+  float* peer_z[8][2] = {};
+  void* peer_ctl[8] = {};
+  void* peer_base[8][3] = {};  // IPC mappings to close
+  uint64_t barriers = 0;
   DeviceBuf trace;  // DEBUG: per-position finalise timestamps (F2V_TRACE)
   DeviceBuf shufR, shufL;  // device Fisher-Yates (f2v_perm.cu)
 
@@ -112,11 +128,23 @@ struct EpochResult {
   double loss;
 };
 void k_prepare_graph(Ctx& c);
-void k_epoch_begin(Ctx& c, uint32_t b, uint32_t s, uint32_t epoch, uint64_t seed, int sampler);
-EpochResult k_epoch_run(Ctx& c, uint32_t b, uint32_t s, float eta, const ForceParams& fp,
-                        bool monitor);
-void k_epoch_restore(Ctx& c, uint32_t b, uint64_t bad_batch);
+void k_shard_layout(Ctx& c, uint32_t batch, uint32_t G);
+void k_epoch_perm(Ctx& c, uint32_t epoch, uint64_t seed);
+void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sampler);
+EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bool monitor);
+void k_epoch_restore(Ctx& c, uint64_t bad_step);
 void k_device_partition(Ctx& c, uint32_t n, uint64_t seed, uint32_t epoch, uint32_t* perm_out);
+void k_device_partition_keyed(Ctx& c, uint32_t n, uint64_t s0, uint32_t* perm_out);
+// host: per-shard ranges/batches and the combined (step, shard) start positions
+void shard_layout(uint32_t n, uint32_t batch, uint32_t G, std::vector<uint32_t>& lo,
+                  std::vector<uint32_t>& bs, std::vector<uint32_t>& nb,
+                  std::vector<uint32_t>& poff, uint32_t& T);
+// multi-process shards (f2v_shard.cu)
+void k_shard_barrier(Ctx& c);
+void k_shard_publish(Ctx& c, uint64_t bad, double loss);
+void k_shard_collect(Ctx& c, uint64_t& bad, double& loss);
+size_t shard_ctl_bytes();
+void k_rows(Ctx& c, uint32_t b, float* rows_dev, bool to_z);  // rows <-> Z[c.ids]
 
 ForceParams make_params(const f2v_force_model& m);
 

@@ -125,12 +125,16 @@ struct Lay {
         if (valid(lane, k, d)) row[col(lane, k)] = v[k];
     }
   }
-  // a Znew row: re-load until no lane sees the sentinel (warp-uniform loop)
+  // a Znew row: re-load until no lane sees the sentinel (warp-uniform loop).
+  // A row that never arrives (a peer GPU died mid-epoch) traps after 2^28
+  // polls (minutes) instead of hanging the device.
   __device__ static __forceinline__ void poll(const float* row, int lane, uint32_t d,
                                               float (&v)[K]) {
+    uint32_t it = 0;
     while (__any_sync(kFull, has_sentinel<K>(v))) {
       __nanosleep(20);
       load(row, lane, d, v, true);
+      if (++it == (1u << 28)) __trap();
     }
   }
   __device__ static __forceinline__ void store(float* row, int lane, uint32_t d,
@@ -529,7 +533,7 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
 struct Rows {
   template <bool ATT, bool RING = false>
-  __device__ static __forceinline__ void run(const ForceParams& fp, uint32_t packed, int cnt,
+  __device__ static __noinline__ void run(const ForceParams& fp, uint32_t packed, int cnt,
                                              int lane, uint32_t d, const float* zold,
                                              const float* znew, const float (&zu)[K],
                                              double (&acc)[K], double& lsum,

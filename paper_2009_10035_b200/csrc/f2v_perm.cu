@@ -92,8 +92,12 @@ __global__ void final_kernel(const uint32_t* __restrict__ succ, const uint32_t* 
 
 // perm_out (device, n entries) = partition_epoch(n, b, Rng::keyed(seed, {0x22, epoch})).perm
 void k_device_partition(Ctx& c, uint32_t n, uint64_t seed, uint32_t epoch, uint32_t* perm_out) {
+  k_device_partition_keyed(c, n, rng_keyed2(seed, kStreamPartition, epoch), perm_out);
+}
+
+// the same shuffle of n elements from a stream whose initial state is s0
+void k_device_partition_keyed(Ctx& c, uint32_t n, uint64_t s0, uint32_t* perm_out) {
   if (n == 0) return;
-  const uint64_t s0 = rng_keyed2(seed, kStreamPartition, epoch);
   const uint32_t N = n - 1;  // steps m = 1 .. n-1
   const size_t nn = std::max<uint32_t>(n, 1);
   c.shufL.ensure(sizeof(uint32_t) * nn * 8);

@@ -1,0 +1,179 @@
+"""GPU parity of the vertex-partitioned G-shard schedule (DESIGN.md
+"Multi-GPU") against the oracle's orc_train(G).
+
+One B200 is available, so the multi-GPU semantics are checked three ways,
+none of which has kernels on one GPU waiting on another process:
+  * the dataflow epoch kernel running ALL G shards of the schedule in one
+    launch (cfg.shards = G) -- the shard ordering, per-shard partitions,
+    per-(step, shard) negatives, step-based windows and first-failure
+    order the multi-GPU kernels execute;
+  * a world-1 ShardedDevice: the IPC-attached path (replica control block,
+    device barriers, failure/loss exchange) with no peers;
+  * the per-step all-gather driver (dist.train_allgather) on the CUDA
+    per-step operators over a world-1 process group.
+Tolerances as in test_gpu_parity.py.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from test_gpu_parity import LOSS_RTOL, kind_model, z_parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev(f2v):
+    d = f2v.Device(0)
+    yield d
+    d.close()
+
+
+def _graph(f2v, orc, n=1500, seed=3):
+    rp, col = orc.orc_sbm_graph(n, 6, 0.03, 0.002, seed)
+    return f2v.CsrGraph(rp, col)
+
+
+@pytest.mark.parametrize("precision", ["fast", "exact"])
+@pytest.mark.parametrize("G,kind,sampler,d,b", [
+    (2, "sigmoid", "philox", 128, 64),
+    (3, "tdist", "splitmix", 128, 50),
+    (8, "tdist", "philox", 64, 32),
+    (4, "sigmoid", "splitmix", 16, 40),
+    (2, "fr", "philox", 2, 64),
+])
+def test_sharded_epochs_match_oracle(f2v, orc, dev, precision, G, kind, sampler, d, b):
+    g = _graph(f2v, orc)
+    n = g.num_vertices()
+    z0 = np.zeros((n, d), np.float32)
+    orc.oracle().orc_random_embedding(n, d, 3, z0)
+    if kind == "fr":
+        z0 *= 0.05
+    mon = kind in ("sigmoid", "tdist")
+    cfg = f2v.TrainConfig(dim=d, batch=b, negatives=5, lr=0.02, epochs=3,
+                          model=kind_model(f2v, kind), seed=9, monitor_loss=mon,
+                          sampler=sampler, precision=precision, shards=G)
+    dev.upload_graph(g)
+    dev.set_embedding(z0)
+    ctr = f2v.TrainCounters()
+    losses = dev.train_epochs(cfg, 0, 1, counters=ctr)
+    z = dev.get_embedding()
+    rc, zr, lr_, cr, _ = orc.orc_train(g.row_offsets, g.col_indices, z0, b, 5, 0.02, 1, kind, 9,
+                                       monitor=mon, sampler=sampler, G=G, threads=8)
+    assert rc == 0
+    z_parity(z, zr)
+    if mon:
+        assert losses[0] == pytest.approx(lr_[0], rel=LOSS_RTOL[precision])
+    assert [ctr.attractive_evals, ctr.repulsive_evals] == [int(cr[0]), int(cr[1])]
+
+
+def test_sharded_trajectory_and_determinism(f2v, orc, dev):
+    """Three epochs run independently on both sides; two device runs are
+    bitwise identical (fixed-order partial combination, no float atomics)."""
+    g = _graph(f2v, orc, 2500, 5)
+    n = g.num_vertices()
+    z0 = np.zeros((n, 128), np.float32)
+    orc.oracle().orc_random_embedding(n, 128, 4, z0)
+    cfg = f2v.TrainConfig(dim=128, batch=96, negatives=5, lr=0.02, epochs=3,
+                          model=kind_model(f2v, "tdist"), seed=2, monitor_loss=True,
+                          sampler="philox", shards=4, lr_decay="linear_to_zero")
+    outs = []
+    for _ in range(2):
+        dev.upload_graph(g)
+        dev.set_embedding(z0)
+        outs.append((dev.train_epochs(cfg), dev.get_embedding()))
+    assert outs[0][0] == outs[1][0] and np.array_equal(outs[0][1], outs[1][1])
+    rc, zr, lr_, _, _ = orc.orc_train(g.row_offsets, g.col_indices, z0, 96, 5, 0.02, 3, "tdist",
+                                      2, sampler="philox", G=4, lr_decay=True, threads=8)
+    assert rc == 0
+    np.testing.assert_allclose(outs[0][0], lr_, rtol=1e-3)
+    rel = np.linalg.norm(outs[0][1].astype(np.float64) - zr) / np.linalg.norm(zr)
+    assert rel < 1e-4, rel
+
+
+def test_sharded_numerical_error_first_failure(f2v, orc, dev):
+    rp, col = orc.orc_sbm_graph(300, 3, 0.1, 0.01, 5)
+    g = f2v.CsrGraph(rp, col)
+    z0 = np.zeros((300, 8), np.float32)
+    orc.oracle().orc_random_embedding(300, 8, 2, z0)
+    z0[123] = 3e37  # FR attraction r^2 overflows fp32 for 123's neighbours
+    cfg = f2v.TrainConfig(dim=8, batch=16, negatives=3, lr=0.02, epochs=2,
+                          model=kind_model(f2v, "fr"), seed=6, shards=3)
+    dev.upload_graph(g)
+    dev.set_embedding(z0)
+    fail = {}
+    with pytest.raises(f2v.NumericalError, match=r"non-finite gradient for vertex \d+ "
+                                                 r"\(epoch 0, batch \d+\)"):
+        dev.train_epochs(cfg, failure=fail)
+    rc, zr, _, _, finfo = orc.orc_train(rp, col, z0, 16, 3, 0.02, 2, "fr", 6, monitor=False, G=3)
+    assert rc == 4
+    assert (fail["epoch"], fail["batch"], fail["vertex"]) == tuple(int(x) for x in finfo)
+    z_parity(dev.get_embedding(), zr)
+
+
+def test_world1_sharded_device_ipc_path(f2v, orc):
+    """ShardedDevice with world 1: attach (own replicas), the per-epoch device
+    barriers and the failure/loss exchange through the control block."""
+    from paper_2009_10035_b200.dist import ShardedDevice
+
+    g = _graph(f2v, orc, 1200, 7)
+    n = g.num_vertices()
+    z0 = np.zeros((n, 128), np.float32)
+    orc.oracle().orc_random_embedding(n, 128, 6, z0)
+    cfg = f2v.TrainConfig(dim=128, batch=128, negatives=5, lr=0.02, epochs=2,
+                          model=kind_model(f2v, "sigmoid"), seed=3, monitor_loss=True,
+                          sampler="philox")
+    sd = ShardedDevice(rank=0, world=1, device=0)
+    try:
+        sd.setup(g, z0)
+        losses = sd.train_epochs(cfg)
+        z = sd.get_embedding()
+        launches = sd.kernel_launches
+    finally:
+        sd.close()
+    rc, zr, lr_, _, _ = orc.orc_train(g.row_offsets, g.col_indices, z0, 128, 5, 0.02, 2,
+                                      "sigmoid", 3, sampler="philox", threads=8)
+    assert rc == 0
+    np.testing.assert_allclose(losses, lr_, rtol=1e-6)
+    rel = np.linalg.norm(z.astype(np.float64) - zr, axis=1) / np.linalg.norm(zr, axis=1)
+    assert rel.max() < 1e-5
+    assert launches > 0
+
+
+def test_allgather_driver_on_device(f2v, orc):
+    """dist.train_allgather over the CUDA per-step operators (world-1 gloo
+    group): per-step grad + failure vote + apply + row exchange."""
+    import torch.distributed as dist
+
+    from paper_2009_10035_b200.dist import DeviceBackend, train_allgather
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        g = _graph(f2v, orc, 900, 2)
+        n = g.num_vertices()
+        z0 = np.zeros((n, 64), np.float32)
+        orc.oracle().orc_random_embedding(n, 64, 8, z0)
+        cfg = f2v.TrainConfig(dim=64, batch=64, negatives=5, lr=0.02, epochs=2,
+                              model=kind_model(f2v, "tdist"), seed=5, monitor_loss=True,
+                              sampler="philox")
+        with f2v.Device(0) as dv:
+            dv.upload_graph(g)
+            dv.set_embedding(z0)
+            losses = train_allgather(DeviceBackend(dv), n, cfg, 0, 1)
+            z = dv.get_embedding()
+            rows = dv.get_rows(np.array([3, 1, 3], np.uint32))
+            assert np.array_equal(rows, z[[3, 1, 3]])
+    finally:
+        dist.destroy_process_group()
+    rc, zr, lr_, _, _ = orc.orc_train(g.row_offsets, g.col_indices, z0, 64, 5, 0.02, 2, "tdist",
+                                      5, sampler="philox", threads=8)
+    assert rc == 0
+    z_parity(z, zr)
+    np.testing.assert_allclose(losses, lr_, rtol=1e-9)
