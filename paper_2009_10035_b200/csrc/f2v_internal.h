@@ -47,7 +47,7 @@ struct EpochTuning {
   uint32_t chunk = 256;  // F2V_CHUNK: max arcs per E item (hub splitting)
   uint32_t lgroup = 8;   // F2V_LGROUP: E chunks per L item
   uint32_t window = 48;  // F2V_WINDOW: arcs to batches [j-window, j) go to L items
-  uint32_t recent = 2;   // F2V_RECENT: window arcs this recent are taken last
+  uint32_t recent = 8;   // F2V_RECENT: window arcs this recent are taken last
   uint32_t lwarps = 2;   // F2V_LWARPS: L-role warps per 8-warp CTA
   uint32_t fast = 1;     // F2V_PRECISION=exact|fast: pair math precision (config)
   uint32_t erecent = 0;  // F2V_ERECENT: chain engine takes arcs of age <= this (0 = off; opt-in)
