@@ -21,6 +21,8 @@ LIB = os.path.join(LIBDIR, "libf2v_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
                      "-Xcompiler", "-O3", "-Xcompiler", "-pthread", "--expt-relaxed-constexpr"]
+if os.environ.get("F2V_NVCC_EXTRA"):  # experiments: e.g. "-DF2V_EPOCH_MINB=3"
+    NVCC_FLAGS += os.environ["F2V_NVCC_EXTRA"].split()
 if os.environ.get("F2V_DEVICE_CHECKS"):  # debug build: device-side bounds checks
     NVCC_FLAGS += ["-DF2V_DEVICE_CHECKS", "-rdc=false"]
 

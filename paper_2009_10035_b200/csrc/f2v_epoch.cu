@@ -30,6 +30,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -217,6 +218,8 @@ void load_tuning(EpochTuning& t) {
   t.lwarps = std::min(uint32_t(ep::kWarps - 1), std::max(1u, env_u32("F2V_LWARPS", t.lwarps)));
   if (const char* e = std::getenv("F2V_PRECISION")) t.fast = std::strcmp(e, "exact") != 0;
   t.erecent = env_u32("F2V_ERECENT", t.erecent);
+  t.ctas = env_u32("F2V_CTAS", t.ctas);
+  t.minb = env_u32("F2V_MINB", t.minb);
   if (t.erecent >= t.window) t.erecent = t.window - 1;
 }
 
@@ -462,7 +465,7 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
     F2V_LAUNCHED(c.stream, "zero_kernel");
     ++c.launches;
   }
-  {  // Znew := sentinel (cudaMalloc'd buffers are 256-byte aligned)
+  auto fill_sentinel = [&] {  // Znew := sentinel (cudaMalloc'd buffers are 256-byte aligned)
     const uint64_t total = uint64_t(c.n) * c.d, n16 = total / 4;
     sentinel_kernel<<<uint32_t(std::min<uint64_t>((n16 + 255) / 256, 4u * c.num_sms * 8)), 256, 0,
                       c.stream>>>(c.z[nxt].as<uint4>(), n16);
@@ -470,7 +473,8 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
     if (total % 4)
       sentinel_tail_kernel<<<1, 4, 0, c.stream>>>(c.z[nxt].as<float>(), n16 * 4, total);
     c.launches += 1;
-  }
+  };
+  fill_sentinel();
   // every replica holds the sentinel before any GPU stores a row into it
   if (multi) k_shard_barrier(c);
   ep::EpochArgs a;
@@ -548,9 +552,60 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
     F2V_CUDA(cudaEventCreate(&c.ev_kernel[0]));
     F2V_CUDA(cudaEventCreate(&c.ev_kernel[1]));
   }
-  F2V_CUDA(cudaEventRecord(c.ev_kernel[0], c.stream));
-  ep::launch_epoch(c, a, monitor, c.tune.fast != 0);
-  F2V_CUDA(cudaEventRecord(c.ev_kernel[1], c.stream));
+  // Occupancy autotune (FAST d = 128): the second epoch of a (graph, config)
+  // (the first one runs cold: fresh buffers, TLB) runs with both register budgets on the same inputs -- the kernel only
+  // reads Zold, so the second run reproduces Znew exactly -- and the faster
+  // build is kept.  Results never depend on the choice (tested).
+  const uint64_t key = (uint64_t(c.n) * 1000003ull + c.nnz) ^ (uint64_t(a.b) << 40) ^
+                       (uint64_t(fp.kind) << 56) ^ (uint64_t(c.shards) << 60) ^
+                       (uint64_t(monitor) << 63);
+  const bool tunable = c.tune.fast && c.d == 128 && !multi;
+  bool tune_now = false;
+  if (c.tune.minb == 2 || c.tune.minb == 3) {
+    c.occ_use = int(c.tune.minb);
+  } else if (!tunable) {
+    c.occ_use = 2;
+  } else if (key != c.occ_key) {
+    c.occ_key = key;
+    c.occ_epochs = 0;
+    c.occ_use = 2;
+  } else if (++c.occ_epochs == 1) {
+    tune_now = true;
+  }
+  auto launch_timed = [&]() {
+    F2V_CUDA(cudaEventRecord(c.ev_kernel[0], c.stream));
+    ep::launch_epoch(c, a, monitor, c.tune.fast != 0);
+    F2V_CUDA(cudaEventRecord(c.ev_kernel[1], c.stream));
+  };
+  if (tune_now) {
+    // load both builds first: with lazy module loading a first launch would
+    // time the load as well
+    c.dry_launch = true;
+    for (int v = 0; v < 2; ++v) {
+      c.occ_use = 2 + v;
+      ep::launch_epoch(c, a, monitor, c.tune.fast != 0);
+    }
+    c.dry_launch = false;
+    float ms[2];
+    for (int v = 0; v < 2; ++v) {
+      if (v) {  // reset the claim counters / first failure, Znew back to the sentinel
+        F2V_CUDA(cudaMemsetAsync(ctr, 0, 8, c.stream));
+        F2V_CUDA(cudaMemsetAsync(ctr + 2, 0xff, 8, c.stream));
+        fill_sentinel();
+      }
+      c.occ_use = 2 + v;
+      launch_timed();
+      F2V_CUDA(cudaEventSynchronize(c.ev_kernel[1]));
+      F2V_CUDA(cudaEventElapsedTime(&ms[v], c.ev_kernel[0], c.ev_kernel[1]));
+      c.occ_ms[v] = ms[v];
+    }
+    c.occ_use = ms[1] < ms[0] ? 3 : 2;
+    if (std::getenv("F2V_DEBUG_OCC"))
+      std::fprintf(stderr, "f2v occupancy autotune: 2 CTAs/SM %.3f ms, 3 CTAs/SM %.3f ms\n", ms[0],
+                   ms[1]);
+  } else {
+    launch_timed();
+  }
   if (monitor) {
     sum_kernel<<<1, 1024, 0, c.stream>>>(c.ploss.as<double>(), c.n,
                                          reinterpret_cast<double*>(ctr + 4));

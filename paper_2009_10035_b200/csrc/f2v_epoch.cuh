@@ -23,6 +23,11 @@ namespace ep {
 using namespace dev;
 
 constexpr int kWarps = 8;       // warps per CTA
+// Register budgets of the epoch kernel (template MINB = resident CTAs per SM
+// it is compiled for): 2 (128 registers, no spills; best when the batch chain
+// dominates) or 3 (80 registers, more gathers in flight; best when bandwidth
+// does).  FAST d = 128 builds both and the driver picks per graph by timing
+// (Ctx::occ_ms); results are identical.
 constexpr int kQ = 64;          // per-warp compaction queue (entries)
 constexpr int kRq = 64;         // per-warp parking lot for the most recent window arcs
 constexpr int kRefs = 32;       // engine: ring refs per vertex (+1 count word); more go global
@@ -504,8 +509,8 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   if (lane == 0) a.vflag[u] = 0;
 }
 
-template <int KIND, int K, bool VEC, bool MON, bool FAST>
-__global__ void __launch_bounds__(kWarps * 32, 2) epoch_kernel(EpochArgs a) {
+template <int KIND, int K, bool VEC, bool MON, bool FAST, int MINB>
+__global__ void __launch_bounds__(kWarps * 32, MINB) epoch_kernel(EpochArgs a) {
   __shared__ uint32_t qs[kWarps][kQ];
   __shared__ uint32_t rs[kWarps][kRq];
   const int lane = threadIdx.x & 31;
@@ -727,11 +732,17 @@ void launch_engine(Ctx& c, const EpochArgs& a) {
 }
 
 // Launch one epoch kernel instantiation as a persistent grid.
-template <int KIND, int K, bool VEC, bool MON, bool FAST>
+template <int KIND, int K, bool VEC, bool MON, bool FAST, int MINB>
 void launch_one(Ctx& c, const EpochArgs& a) {
-  auto kern = epoch_kernel<KIND, K, VEC, MON, FAST>;
+  auto kern = epoch_kernel<KIND, K, VEC, MON, FAST, MINB>;
+  if (c.dry_launch) {  // load the function only (CUDA lazy loading) -- no launch
+    cudaFuncAttributes fa;
+    F2V_CUDA(cudaFuncGetAttributes(&fa, kern));
+    return;
+  }
   int per_sm = 0;
   F2V_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0));
+  if (c.tune.ctas && int(c.tune.ctas) < per_sm) per_sm = int(c.tune.ctas);
   if (per_sm < 1) per_sm = 1;
   uint32_t blocks = uint32_t(per_sm) * uint32_t(c.num_sms);
   if (a.Re) {
@@ -758,8 +769,15 @@ void launch_one(Ctx& c, const EpochArgs& a) {
 
 template <int KIND, int K, bool VEC, bool FAST>
 void launch_mon(Ctx& c, const EpochArgs& a, bool mon) {
-  if (mon) launch_one<KIND, K, VEC, true, FAST>(c, a);
-  else launch_one<KIND, K, VEC, false, FAST>(c, a);
+  if constexpr (FAST && K == 4) {
+    if (c.occ_use == 3) {
+      if (mon) launch_one<KIND, K, VEC, true, FAST, 3>(c, a);
+      else launch_one<KIND, K, VEC, false, FAST, 3>(c, a);
+      return;
+    }
+  }
+  if (mon) launch_one<KIND, K, VEC, true, FAST, 2>(c, a);
+  else launch_one<KIND, K, VEC, false, FAST, 2>(c, a);
 }
 
 template <int K, bool VEC, bool FAST>

@@ -5,8 +5,8 @@
 namespace f2v {
 namespace ep {
 void launch_exact_any_k32(Ctx& c, const EpochArgs& a, bool mon) {
-  if (mon) launch_one<-1, 32, false, true, false>(c, a);
-  else launch_one<-1, 32, false, false, false>(c, a);
+  if (mon) launch_one<-1, 32, false, true, false, 2>(c, a);
+  else launch_one<-1, 32, false, false, false, 2>(c, a);
 }
 }  // namespace ep
 }  // namespace f2v

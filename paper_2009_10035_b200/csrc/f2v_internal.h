@@ -50,6 +50,8 @@ struct EpochTuning {
   uint32_t recent = 8;   // F2V_RECENT: window arcs this recent are taken last
   uint32_t lwarps = 2;   // F2V_LWARPS: L-role warps per 8-warp CTA
   uint32_t fast = 1;     // F2V_PRECISION=exact|fast: pair math precision (config)
+  uint32_t ctas = 0;     // F2V_CTAS: resident epoch CTAs per SM (0 = as many as fit)
+  uint32_t minb = 0;     // F2V_MINB: epoch register budget 2 or 3 CTAs/SM (0 = autotune)
   uint32_t erecent = 0;  // F2V_ERECENT: chain engine takes arcs of age <= this (0 = off; opt-in)
 };
 void load_tuning(EpochTuning& t);
@@ -89,6 +91,13 @@ struct Ctx {
   cudaStream_t stream2 = nullptr;                 // the chain engine runs here
   cudaEvent_t ev_prep = nullptr, ev_engine = nullptr;
   uint32_t eff_re = 0, eff_maxe = 0;              // engine window / ring rows this epoch
+  // occupancy autotune (FAST d = 128): kernel ms of the 2- and 3-CTA builds on
+  // this graph + config (negative = not yet timed) and the build in use
+  double occ_ms[2] = {-1.0, -1.0};
+  uint64_t occ_key = 0;
+  uint32_t occ_epochs = 0;
+  bool dry_launch = false;  // launch_epoch only loads the selected kernel
+  int occ_use = 2;
   // vertex shards: G shards, step-major combined order
   uint32_t shards = 1;        // G of the current run
   int32_t rank = -1;          // this process's shard; -1 = one process runs every shard

@@ -459,6 +459,59 @@ __device__ __forceinline__ int lane_of_pair(int i) {
   return (((i >> 2) & 1) << 4) | (((i >> 1) & 1) << 3) | ((i & 1) << 2);
 }
 
+// One block of 8 loaded rows w (pairs k0..k0+7 of the call): transposed
+// reduction, force term, fp32 axpy of the block, fp64 accumulate.
+template <int KIND, int K, bool MON, bool ATT>
+__device__ __forceinline__ void fast_block(const ForceParams& fp, int k0, int cnt, int lane,
+                                           const float (&zu)[K], float (&w)[8][K],
+                                           double (&acc)[K], double& lsum) {
+  constexpr bool SIG = KIND == F2V_SIGMOID;
+  const int pi = pair_of_lane(lane);
+  float part[8], nrm[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float s = 0.f, q = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (SIG) {
+        s = fmaf(zu[k], w[i][k], s);
+        if (!ATT) q = fmaf(w[i][k], w[i][k], q);
+      } else {
+        w[i][k] = zu[k] - w[i][k];
+        s = fmaf(w[i][k], w[i][k], s);
+      }
+    }
+    part[i] = s;
+    nrm[i] = q;
+  }
+  const float red = reduce8(part, lane);
+  const float nr = (SIG && !ATT) ? reduce8(nrm, lane) : 0.f;
+  const FastTerm t = fast_term<KIND, ATT, MON>(fp, red, nr);
+  if (MON && (lane & 3) == 0 && k0 + pi < cnt) lsum = __dadd_rn(lsum, double(t.loss));
+  float a32[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) a32[k] = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float qi = __shfl_sync(kFull, t.q, lane_of_pair(i));
+    const float fbi = SIG ? 0.f : __shfl_sync(kFull, t.fb, lane_of_pair(i));
+    if (k0 + i < cnt) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) a32[k] = fmaf(qi, w[i][k], a32[k]);
+      if (!SIG && lane == 0) a32[0] += fbi;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = __dadd_rn(acc[k], double(a32[k]));
+}
+
+#ifndef F2V_FAST_INFLIGHT
+#define F2V_FAST_INFLIGHT 8  // row gathers in flight per warp (8; 16 measured slower)
+#endif
+
+// The rows of one call are gathered NB = F2V_FAST_INFLIGHT at a time (all
+// loads issued before any block is reduced: 16 x 512 B in flight per warp),
+// then reduced 8 at a time in order.
 template <int KIND, int K, bool MON, bool ATT, bool RING = false>
 __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed, int cnt,
                                           int lane, uint32_t d, const float* __restrict__ zold,
@@ -466,66 +519,35 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
                                           double (&acc)[K], double& lsum,
                                           const float* ring = nullptr) {
   using L = Lay<K, true>;
-  constexpr bool SIG = KIND == F2V_SIGMOID;
-  const int pi = pair_of_lane(lane);
-  for (int k0 = 0; k0 < cnt; k0 += 8) {
-    float w[8][K];
-    uint32_t pks[8];
+  constexpr int NB = F2V_FAST_INFLIGHT;
+  for (int k0 = 0; k0 < cnt; k0 += NB) {
+    float w[NB / 8][8][K];
+    uint32_t pks[NB];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < NB; ++i) {
       const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
       pks[i] = pk;
       if (k0 + i < cnt) {
         const bool coh = (pk & kNewBit) != 0;
         if (RING && (pk & kRingBit))
-          L::load_smem(ring + size_t(pk & kIdMask) * d, lane, d, w[i]);
+          L::load_smem(ring + size_t(pk & kIdMask) * d, lane, d, w[i / 8][i % 8]);
         else
-          L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, w[i], coh);
+          L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, w[i / 8][i % 8],
+                  coh);
       } else {
 #pragma unroll
-        for (int k = 0; k < K; ++k) w[i][k] = 0.0f;
+        for (int k = 0; k < K; ++k) w[i / 8][i % 8][k] = 0.0f;
       }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i)  // Znew rows not yet final: poll
-      if (k0 + i < cnt && (pks[i] & kNewBit) && !(RING && (pks[i] & kRingBit)))
-        L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, w[i]);
-    float part[8], nrm[8];
+    for (int h = 0; h < NB / 8; ++h) {
+      if (k0 + 8 * h >= cnt) break;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float s = 0.f, q = 0.f;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        if (SIG) {
-          s = fmaf(zu[k], w[i][k], s);
-          if (!ATT) q = fmaf(w[i][k], w[i][k], q);
-        } else {
-          w[i][k] = zu[k] - w[i][k];
-          s = fmaf(w[i][k], w[i][k], s);
-        }
-      }
-      part[i] = s;
-      nrm[i] = q;
+      for (int i = 8 * h; i < 8 * h + 8; ++i)  // Znew rows not yet final: poll
+        if (k0 + i < cnt && (pks[i] & kNewBit) && !(RING && (pks[i] & kRingBit)))
+          L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, w[h][i % 8]);
+      fast_block<KIND, K, MON, ATT>(fp, k0 + 8 * h, cnt, lane, zu, w[h], acc, lsum);
     }
-    const float red = reduce8(part, lane);
-    const float nr = (SIG && !ATT) ? reduce8(nrm, lane) : 0.f;
-    const FastTerm t = fast_term<KIND, ATT, MON>(fp, red, nr);
-    if (MON && (lane & 3) == 0 && k0 + pi < cnt) lsum = __dadd_rn(lsum, double(t.loss));
-    float a32[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) a32[k] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const float qi = __shfl_sync(kFull, t.q, lane_of_pair(i));
-      const float fbi = SIG ? 0.f : __shfl_sync(kFull, t.fb, lane_of_pair(i));
-      if (k0 + i < cnt) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) a32[k] = fmaf(qi, w[i][k], a32[k]);
-        if (!SIG && lane == 0) a32[0] += fbi;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = __dadd_rn(acc[k], double(a32[k]));
   }
 }
 

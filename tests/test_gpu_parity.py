@@ -432,3 +432,28 @@ def test_device_fisher_yates_bit_exact(f2v, dev, n, b):
     for seed, epoch in [(1, 0), (99, 7)]:
         assert np.array_equal(dev.partition_epoch(n, b, seed, epoch),
                               f2v.partition_epoch(n, b, seed, epoch))
+
+
+def test_occupancy_builds_bitwise_identical(f2v, orc):
+    """The 2- and 3-CTA/SM register budgets of the FAST d=128 kernel (the
+    per-graph autotune picks one) give bitwise identical epochs."""
+    g = f2v.rmat_graph(12, 16, seed=3)
+    n = g.num_vertices()
+    z0 = np.zeros((n, 128), np.float32)
+    orc.oracle().orc_random_embedding(n, 128, 2, z0)
+    cfg = f2v.TrainConfig(dim=128, batch=128, negatives=5, lr=0.02, epochs=2,
+                          model=kind_model(f2v, "sigmoid"), seed=3, monitor_loss=True,
+                          sampler="philox")
+    outs = []
+    for minb in ("2", "3", "0"):
+        os.environ["F2V_MINB"] = minb
+        try:
+            dev = f2v.Device(0)
+        finally:
+            del os.environ["F2V_MINB"]
+        dev.upload_graph(g)
+        dev.set_embedding(z0)
+        outs.append((dev.train_epochs(cfg), dev.get_embedding()))
+        dev.close()
+    for l, z in outs[1:]:
+        assert l == outs[0][0] and np.array_equal(z, outs[0][1])
