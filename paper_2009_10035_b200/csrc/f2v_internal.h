@@ -48,7 +48,7 @@ struct EpochTuning {
   uint32_t lgroup = 8;   // F2V_LGROUP: E chunks per L item
   uint32_t window = 48;  // F2V_WINDOW: arcs to batches [j-window, j) go to L items
   uint32_t recent = 8;   // F2V_RECENT: window arcs this recent are taken last
-  uint32_t lwarps = 2;   // F2V_LWARPS: L-role warps per 8-warp CTA
+  uint32_t lwarps = 1;   // F2V_LWARPS: L-role warps per 8-warp CTA
   uint32_t fast = 1;     // F2V_PRECISION=exact|fast: pair math precision (config)
   uint32_t ctas = 0;     // F2V_CTAS: resident epoch CTAs per SM (0 = as many as fit)
   uint32_t minb = 0;     // F2V_MINB: epoch register budget 2 or 3 CTAs/SM (0 = autotune)
