@@ -82,6 +82,10 @@ typedef struct {
                             context attached to peers (f2v_shard_attach) G = the world
                             size and each GPU runs its own shard; otherwise one GPU runs
                             all G shards (same results). */
+  uint32_t walk_length;  /* SampleMode (sampling.hpp:12-20): 0 = one-hop (CSR neighbours),
+                            k > 0 = walk mode: the context of u is a k-step random walk
+                            (gen_walk, sampling.cpp:27-41) drawn on the batch stream before
+                            the negatives; attractive_evals = k per non-isolated vertex */
 } f2v_train_config;
 
 /* TrainCounters, trainer.hpp:83-87 */

@@ -390,13 +390,51 @@ void orc_shard_range(uint32_t n, uint32_t G, uint32_t g, uint32_t* lo, uint32_t*
   *hi = (uint32_t)((uint64_t)n * (g + 1) / G);
 }
 
+/* gen_walk (sampling.cpp:27-41): k steps from u on the stream st (one below()
+ * per step); a dead end restarts at u; an isolated u yields no walk. */
+static void orc_gen_walk(const uint64_t* rowptr, const uint32_t* col, uint32_t u, uint32_t k,
+                         uint64_t* st, uint32_t* out) {
+  if (rowptr[u + 1] == rowptr[u]) return;
+  uint32_t w = u;
+  for (uint32_t i = 0; i < k; ++i) {
+    if (rowptr[w + 1] == rowptr[w]) w = u; /* dead end: restart */
+    const uint64_t deg = rowptr[w + 1] - rowptr[w];
+    const uint32_t next = col[rowptr[w] + orc_rng_below(st, deg)];
+    out[i] = next;
+    w = next;
+  }
+}
+
 int orc_train(const uint64_t* rowptr, const uint32_t* col, uint32_t n, float* z,
               uint32_t d, uint32_t batch, uint32_t s, float lr, uint32_t epochs,
               int kind, float eps, float cap, uint64_t seed, int lr_decay, int monitor,
               int sampler, uint32_t G, int threads, double* loss_out,
               uint64_t* counters, orc_step_cb cb, void* user, uint32_t* fail_info) {
+  return orc_train_mode(rowptr, col, n, z, d, batch, s, lr, epochs, kind, eps, cap, seed,
+                        lr_decay, monitor, sampler, G, 0, threads, loss_out, counters, cb, user,
+                        fail_info);
+}
+
+int orc_train_mode(const uint64_t* rowptr, const uint32_t* col, uint32_t n, float* z,
+                   uint32_t d, uint32_t batch, uint32_t s, float lr, uint32_t epochs,
+                   int kind, float eps, float cap, uint64_t seed, int lr_decay, int monitor,
+                   int sampler, uint32_t G, uint32_t walk_k, int threads, double* loss_out,
+                   uint64_t* counters, orc_step_cb cb, void* user, uint32_t* fail_info) {
   if (d < 1 || batch < 1 || s < 1 || !(lr > 0) || epochs < 1 || G < 1 || n < G)
     return 1; /* TrainConfig::validate, trainer.cpp:13-22 */
+  /* walk mode (SampleMode::walk(k), sampling.hpp:12-20): the context of u is
+   * its k-step walk; layout: ctx row u at k * (non-isolated vertices < u) */
+  uint64_t* cptr = NULL;
+  uint32_t* ccol = NULL;
+  if (walk_k) {
+    cptr = (uint64_t*)malloc(sizeof(uint64_t) * ((size_t)n + 1));
+    cptr[0] = 0;
+    for (uint32_t u = 0; u < n; ++u)
+      cptr[u + 1] = cptr[u] + (rowptr[u + 1] > rowptr[u] ? walk_k : 0);
+    ccol = (uint32_t*)malloc(sizeof(uint32_t) * (cptr[n] ? cptr[n] : 1));
+  }
+  const uint64_t* xptr = walk_k ? cptr : rowptr; /* the context CSR */
+  const uint32_t* xcol = walk_k ? ccol : col;
   if (monitor && kind != ORC_SIGMOID && kind != ORC_TDIST) return 6;
   uint32_t* perms = (uint32_t*)malloc(sizeof(uint32_t) * n);
   uint32_t* lo = (uint32_t*)malloc(sizeof(uint32_t) * G);
@@ -432,13 +470,21 @@ int orc_train(const uint64_t* rowptr, const uint32_t* col, uint32_t n, float* z,
     for (uint64_t t = 0; t < T && rc == 0; ++t) {
       /* negatives per shard (sampling.cpp:59) */
       for (uint32_t g = 0; g < G; ++g) {
+        /* build_minibatch (sampling.cpp:43-61): walks (walk mode) then the
+         * negatives, on one stream (seed,{0x33,epoch,t[,g]}) */
+        const uint64_t key3[3] = {0x33, epoch, t}, key4[4] = {0x33, epoch, t, g};
+        uint64_t st = G == 1 ? orc_rng_keyed(seed, key3, 3) : orc_rng_keyed(seed, key4, 4);
+        if (walk_k && t < nb[g]) {
+          uint32_t l, h;
+          orc_shard_range(n, G, g, &l, &h);
+          const uint32_t p0 = l + (uint32_t)(t * bs[g]);
+          const uint32_t p1 = (uint32_t)((uint64_t)p0 + bs[g] < h ? p0 + bs[g] : h);
+          for (uint32_t p = p0; p < p1; ++p)
+            orc_gen_walk(rowptr, col, perms[p], walk_k, &st, ccol + cptr[perms[p]]);
+        }
         if (sampler == 1) {
           orc_philox_negatives(seed, epoch, t, g, n, s, negs + (size_t)g * s);
-        } else if (G == 1) {
-          orc_ref_negatives(seed, epoch, t, n, s, negs);
         } else {
-          const uint64_t key[4] = {0x33, epoch, t, g};
-          uint64_t st = orc_rng_keyed(seed, key, 4);
           for (uint32_t k = 0; k < s; ++k) negs[g * s + k] = (uint32_t)orc_rng_below(&st, n);
         }
       }
@@ -450,7 +496,7 @@ int orc_train(const uint64_t* rowptr, const uint32_t* col, uint32_t n, float* z,
         const uint32_t p0 = l + (uint32_t)(t * bs[g]);
         const uint32_t p1 = (uint32_t)((uint64_t)p0 + bs[g] < h ? p0 + bs[g] : h);
         uint32_t bad = 0;
-        const int r = orc_grad_minibatch(rowptr, col, n, z, d, perms + p0, p1 - p0,
+        const int r = orc_grad_minibatch(xptr, xcol, n, z, d, perms + p0, p1 - p0,
                                          negs + (size_t)g * s, s, kind, eps, cap, threads,
                                          grads + (size_t)g * bmax * d, &bad);
         if (r) {
@@ -458,11 +504,11 @@ int orc_train(const uint64_t* rowptr, const uint32_t* col, uint32_t n, float* z,
           if (fail_info) { fail_info[0] = epoch; fail_info[1] = (uint32_t)t; fail_info[2] = bad; }
           break;
         }
-        for (uint32_t p = p0; p < p1; ++p) attr += rowptr[perms[p] + 1] - rowptr[perms[p]];
+        for (uint32_t p = p0; p < p1; ++p) attr += xptr[perms[p] + 1] - xptr[perms[p]];
         rep += (uint64_t)(p1 - p0) * s;
         if (monitor) {
           double l2 = 0.0;
-          orc_batch_loss(rowptr, col, z, d, perms + p0, p1 - p0, negs + (size_t)g * s, s,
+          orc_batch_loss(xptr, xcol, z, d, perms + p0, p1 - p0, negs + (size_t)g * s, s,
                          kind, eps, cap, &l2);
           epoch_loss += l2;
         }
@@ -481,6 +527,6 @@ int orc_train(const uint64_t* rowptr, const uint32_t* col, uint32_t n, float* z,
     if (rc == 0 && monitor && loss_out) loss_out[epoch] = epoch_loss;
   }
   if (counters) { counters[0] = attr; counters[1] = rep; }
-  free(perms); free(lo); free(bs); free(nb); free(negs); free(grads);
+  free(perms); free(lo); free(bs); free(nb); free(negs); free(grads); free(cptr); free(ccol);
   return rc;
 }

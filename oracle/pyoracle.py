@@ -80,6 +80,11 @@ def oracle():
                                      C.c_uint32, C.c_float, C.c_uint32, C.c_int, C.c_float,
                                      C.c_float, C.c_uint64, C.c_int, C.c_int, C.c_int,
                                      C.c_uint32, C.c_int, f64p, u64p, STEP_CB, C.c_void_p, u32p])
+        _sig(L, "orc_train_mode", C.c_int, [u64p, u32p, C.c_uint32, f32p, C.c_uint32,
+                                          C.c_uint32, C.c_uint32, C.c_float, C.c_uint32, C.c_int,
+                                          C.c_float, C.c_float, C.c_uint64, C.c_int, C.c_int,
+                                          C.c_int, C.c_uint32, C.c_uint32, C.c_int, f64p, u64p,
+                                          STEP_CB, C.c_void_p, u32p])
         _sig(L, "orc_shard_range", None, [C.c_uint32, C.c_uint32, C.c_uint32,
                                         C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)])
         _orc = L
@@ -139,6 +144,14 @@ def reference():
                                      C.c_float, C.c_uint32, C.c_int, C.c_float, C.c_float,
                                      C.c_uint64, C.c_uint32, C.c_int, C.c_int, C.c_void_p,
                                      C.c_void_p, f64p, u64p, C.c_void_p, C.c_void_p, u32p])
+        _sig(L, "ref_train_mode", C.c_int, [C.c_void_p, f32p, C.c_uint32, C.c_uint32,
+                                          C.c_uint32, C.c_float, C.c_uint32, C.c_int, C.c_float,
+                                          C.c_float, C.c_uint64, C.c_uint32, C.c_int, C.c_int,
+                                          C.c_uint32, C.c_void_p, C.c_void_p, f64p, u64p,
+                                          C.c_void_p, C.c_void_p, u32p])
+        _sig(L, "ref_walk_minibatch", C.c_int, [C.c_void_p, u32p, C.c_uint32, C.c_uint32,
+                                              C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64,
+                                              u64p, u32p, u32p])
         _sig(L, "ref_train_stock", C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32,
                                            C.c_float, C.c_uint32, C.c_int, C.c_uint64,
                                            C.c_uint32, C.c_int, f32p, f64p])
@@ -284,7 +297,7 @@ def orc_batch_loss(rowptr, col, z, ids, negs, kind, eps=1e-6, cap=5.0):
 
 def orc_train(rowptr, col, z0, batch, s, lr, epochs, kind, seed, eps=1e-6, cap=5.0,
               lr_decay=False, monitor=True, sampler="splitmix", G=1, threads=4,
-              step_cb=None):
+              step_cb=None, walk=0):
     """The train() loop (trainer.cpp:192-251) with injected Z0.  Returns
     (rc, Z, epoch_losses, counters, fail_info)."""
     z = np.array(z0, np.float32, copy=True, order="C")
@@ -299,8 +312,8 @@ def orc_train(rowptr, col, z0, batch, s, lr, epochs, kind, seed, eps=1e-6, cap=5
     else:
         cb = STEP_CB()
     colc = np.ascontiguousarray(col if len(col) else np.zeros(1, np.uint32), np.uint32)
-    rc = oracle().orc_train(np.ascontiguousarray(rowptr, np.uint64), colc, n, z, d, batch, s,
-                            lr, epochs, KINDS.get(kind, kind), eps, cap, seed, int(lr_decay),
-                            int(monitor), 1 if sampler in ("philox", 1) else 0, G, threads,
-                            losses, counters, cb, None, fail)
+    rc = oracle().orc_train_mode(np.ascontiguousarray(rowptr, np.uint64), colc, n, z, d, batch,
+                                 s, lr, epochs, KINDS.get(kind, kind), eps, cap, seed,
+                                 int(lr_decay), int(monitor), 1 if sampler in ("philox", 1) else 0,
+                                 G, walk, threads, losses, counters, cb, None, fail)
     return rc, z, losses, counters, fail

@@ -287,12 +287,32 @@ int ref_batch_negatives(void* gp, std::uint64_t seed, std::uint32_t epoch,
 // step_cb (nullable) is called after each apply_update with (epoch, batch).
 typedef void (*ref_step_cb)(std::uint32_t epoch, std::uint64_t batch, const float* z,
                             void* user);
+int ref_train_mode(void* gp, float* z, std::uint32_t d, std::uint32_t batch,
+                   std::uint32_t s, float lr, std::uint32_t epochs, int kind, float eps,
+                   float cap, std::uint64_t seed, std::uint32_t workers, int lr_decay,
+                   int monitor, std::uint32_t walk_k, const std::uint32_t* perm_in,
+                   const std::uint32_t* negs_in, double* loss_out, std::uint64_t* counters,
+                   ref_step_cb cb, void* user, std::uint32_t* fail_info);
+
 int ref_train(void* gp, float* z, std::uint32_t d, std::uint32_t batch,
               std::uint32_t s, float lr, std::uint32_t epochs, int kind, float eps,
               float cap, std::uint64_t seed, std::uint32_t workers, int lr_decay,
               int monitor, const std::uint32_t* perm_in, const std::uint32_t* negs_in,
               double* loss_out, std::uint64_t* counters, ref_step_cb cb, void* user,
               std::uint32_t* fail_info /*[3]: epoch, batch, vertex*/) {
+  return ref_train_mode(gp, z, d, batch, s, lr, epochs, kind, eps, cap, seed, workers, lr_decay,
+                        monitor, 0, perm_in, negs_in, loss_out, counters, cb, user, fail_info);
+}
+
+// ref_train with the reference's SampleMode: walk_k > 0 = SampleMode::walk(k)
+// (build_minibatch draws the walks, then the negatives; injected negs_in
+// replace only the negatives).
+int ref_train_mode(void* gp, float* z, std::uint32_t d, std::uint32_t batch,
+                   std::uint32_t s, float lr, std::uint32_t epochs, int kind, float eps,
+                   float cap, std::uint64_t seed, std::uint32_t workers, int lr_decay,
+                   int monitor, std::uint32_t walk_k, const std::uint32_t* perm_in,
+                   const std::uint32_t* negs_in, double* loss_out, std::uint64_t* counters,
+                   ref_step_cb cb, void* user, std::uint32_t* fail_info) {
   const CsrGraph& g = *static_cast<CsrGraph*>(gp);
   const VertexId n = g.num_vertices();
   std::uint32_t cur_epoch = 0;
@@ -323,7 +343,8 @@ int ref_train(void* gp, float* z, std::uint32_t d, std::uint32_t batch,
         cur_batch = bi;
         const auto ids = part.batch(bi);
         Minibatch mb;
-        if (negs_in) {
+        const SampleMode mode = walk_k ? SampleMode::walk(walk_k) : SampleMode::one_hop();
+        if (negs_in && !walk_k) {
           mb.vertices.assign(ids.begin(), ids.end());
           const std::uint32_t* p = negs_in + (std::size_t(epoch) * nb + bi) * s;
           mb.negatives.assign(p, p + s);
@@ -331,7 +352,11 @@ int ref_train(void* gp, float* z, std::uint32_t d, std::uint32_t batch,
           mb.graph = &g;
         } else {
           Rng batch_rng = Rng::keyed(seed, {0x33, epoch, bi});
-          mb = build_minibatch(g, ids, SampleMode::one_hop(), s, batch_rng);
+          mb = build_minibatch(g, ids, mode, s, batch_rng);
+          if (negs_in) {
+            const std::uint32_t* p = negs_in + (std::size_t(epoch) * nb + bi) * s;
+            mb.negatives.assign(p, p + s);
+          }
         }
         BatchSchedule sched = make_schedule(g, ids, workers, true);
         grad_minibatch(g, zm, mb, model, sched, grads, &tc);
@@ -348,6 +373,24 @@ int ref_train(void* gp, float* z, std::uint32_t d, std::uint32_t batch,
     if (fail_info) { fail_info[0] = cur_epoch; fail_info[1] = std::uint32_t(cur_batch); }
     return classify(e);
   }
+}
+
+// build_minibatch in walk mode for one batch: the walks (ctx_offsets / ctx_ids,
+// sampling.cpp:27-41,50-58) and then the negatives on (seed,{0x33,epoch,bi}).
+int ref_walk_minibatch(void* gp, const std::uint32_t* ids, std::uint32_t b, std::uint32_t k,
+                       std::uint32_t s, std::uint64_t seed, std::uint32_t epoch,
+                       std::uint64_t bi, std::uint64_t* offs_out, std::uint32_t* ctx_out,
+                       std::uint32_t* negs_out) {
+  try {
+    const CsrGraph& g = *static_cast<CsrGraph*>(gp);
+    Rng rng = Rng::keyed(seed, {0x33, epoch, bi});
+    Minibatch mb = build_minibatch(g, std::span<const VertexId>(ids, b), SampleMode::walk(k), s,
+                                   rng);
+    for (std::size_t i = 0; i <= b; ++i) offs_out[i] = mb.ctx_offsets[i];
+    std::memcpy(ctx_out, mb.ctx_ids.data(), sizeof(std::uint32_t) * mb.ctx_ids.size());
+    std::memcpy(negs_out, mb.negatives.data(), sizeof(std::uint32_t) * s);
+    return 0;
+  } catch (const std::exception& e) { return classify(e); }
 }
 
 // The unmodified train() (init U(-0.5/d, 0.5/d), its own streams).

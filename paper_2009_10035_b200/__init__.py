@@ -83,7 +83,8 @@ class _TrainConfig(C.Structure):
                 ("lr", C.c_float), ("epochs", C.c_uint32), ("model", _ForceModel),
                 ("seed", C.c_uint64), ("lr_decay", C.c_int32), ("monitor_loss", C.c_int32),
                 ("sampler", C.c_int32), ("init", C.c_int32), ("first_epoch", C.c_uint32),
-                ("run_epochs", C.c_uint32), ("precision", C.c_int32), ("shards", C.c_uint32)]
+                ("run_epochs", C.c_uint32), ("precision", C.c_int32), ("shards", C.c_uint32),
+                ("walk_length", C.c_uint32)]
 
 
 class _Counters(C.Structure):
@@ -232,6 +233,7 @@ class TrainConfig:
     sampler: str = "splitmix"
     precision: str = "fast"  # "fast" (fp32 pair math, fp64 accumulate) or "exact" (fp64)
     shards: int = 1  # vertex shards G; 1 = the reference's stream
+    walk_length: int = 0  # SampleMode: 0 one-hop, k > 0 walk mode (sampling.hpp:12-20)
 
     def _c(self, init: int = 0, first_epoch: int = 0, run_epochs: int = 0) -> _TrainConfig:
         if self.lr_decay not in ("constant", "linear_to_zero"):
@@ -246,7 +248,8 @@ class TrainConfig:
                             self.model._c(), self.seed & (2**64 - 1),
                             int(self.lr_decay == "linear_to_zero"), int(self.monitor_loss),
                             SAMPLERS[self.sampler], init, first_epoch, run_epochs,
-                            0 if self.precision == "fast" else 1, int(self.shards))
+                            0 if self.precision == "fast" else 1, int(self.shards),
+                            int(self.walk_length))
 
 
 @dataclasses.dataclass

@@ -170,6 +170,7 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
   if (c.n >= 0x80000000u) fail(F2V_EUSAGE, "n must be < 2^31");
   if (cfg.precision != F2V_PRECISION_FAST && cfg.precision != F2V_PRECISION_EXACT)
     fail(F2V_EUSAGE, "unknown precision");
+  if (cfg.walk_length > 1024) fail(F2V_EUSAGE, "walk length must be <= 1024");
   const char* penv = std::getenv("F2V_PRECISION");  // test/debug override
   c.tune.fast = penv ? (std::strcmp(penv, "exact") != 0) : cfg.precision == F2V_PRECISION_FAST;
   if (cfg.init == 1) {
@@ -192,12 +193,14 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
     if (G != c.world) fail(F2V_EUSAGE, "cfg.shards must equal the number of attached GPUs");
   }
   k_shard_layout(c, cfg.batch, G);  // batch clamped per shard (trainer.cpp:200)
+  k_set_context(c, cfg.walk_length);  // SampleMode: one-hop CSR or k-step walks
   uint64_t attr = 0, rep = 0;
   for (uint32_t e = cfg.first_epoch; e < end_epoch; ++e) {
     float eta = cfg.lr;
     if (cfg.lr_decay) eta = cfg.lr * (1.0f - float(e) / float(cfg.epochs));
     // partition_epoch (trainer.cpp:216-217) as a device Fisher-Yates per shard
     k_epoch_perm(c, e, cfg.seed);
+    if (c.walk_k) k_epoch_walks(c, e, cfg.seed);  // build_minibatch's walks (sampling.cpp:50-58)
     k_epoch_begin(c, s, e, cfg.seed, cfg.sampler);
     const EpochResult r = k_epoch_run(c, s, eta, fp, cfg.monitor_loss != 0);
     if (r.bad_pos != ~0ull) {
@@ -275,7 +278,7 @@ void f2v_destroy(f2v_ctx* h) {
         &c.state, &c.negs_all, &c.negwin, &c.items, &c.litems, &c.nE, &c.nL, &c.EP, &c.LP,
         &c.wtot, &c.needs, &c.scan_tmp, &c.epart, &c.eloss, &c.wcnt, &c.wl, &c.lpart, &c.lloss,
         &c.ploss, &c.counters, &c.trace, &c.shufR, &c.shufL, &c.nEng, &c.ecum, &c.epos,
-        &c.eslot, &c.eidx, &c.rcnt, &c.poff, &c.lperm})
+        &c.eslot, &c.eidx, &c.rcnt, &c.poff, &c.lperm, &c.grow, &c.gcol, &c.wflag, &c.wpos})
     b->release();
   for (uint32_t g = 0; g < 8; ++g)  // peers' replicas mapped by f2v_shard_attach
     for (int i = 0; i < 3; ++i)
@@ -325,6 +328,12 @@ int32_t f2v_upload_graph(f2v_ctx* h, uint32_t n, const uint64_t* row_offsets,
     F2V_CUDA(cudaSetDevice(c.device));
     if (row_offsets[0] != 0 || row_offsets[n] != nnz)
       fail(F2V_ERANGE, "row_offsets inconsistent with nnz");
+    if (c.walk_k) {  // drop a walk context of the previous graph
+      c.grow.release();
+      c.gcol.release();
+      c.h_growptr.clear();
+      c.walk_k = 0;
+    }
     c.n = n;
     c.nnz = nnz;
     c.h_rowptr.assign(row_offsets, row_offsets + n + 1);
@@ -397,6 +406,7 @@ int32_t f2v_grad_minibatch(f2v_ctx* h, const uint32_t* ids, uint32_t b, const ui
   return guard(&h->c, [&] {
     Ctx& c = h->c;
     need_graph(c);
+    k_set_context(c, 0);  // per-step operators take one-hop minibatches
     need_embedding(c);
     validate_model(model);
     F2V_CUDA(cudaSetDevice(c.device));
@@ -449,6 +459,7 @@ int32_t f2v_batch_loss(f2v_ctx* h, const uint32_t* ids, uint32_t b, const uint32
   return guard(&h->c, [&] {
     Ctx& c = h->c;
     need_graph(c);
+    k_set_context(c, 0);  // per-step operators take one-hop minibatches
     need_embedding(c);
     validate_model(model);
     if (model.kind != F2V_SIGMOID && model.kind != F2V_TDIST)
@@ -467,6 +478,7 @@ int32_t f2v_step(f2v_ctx* h, const uint32_t* ids, uint32_t b, const uint32_t* ne
   return guard(&h->c, [&] {
     Ctx& c = h->c;
     need_graph(c);
+    k_set_context(c, 0);  // per-step operators take one-hop minibatches
     need_embedding(c);
     validate_model(model);
     const bool mon = loss_out != nullptr;

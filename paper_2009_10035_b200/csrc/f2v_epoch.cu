@@ -153,17 +153,22 @@ __global__ void engine_emit_kernel(const uint32_t* __restrict__ ecum,
 __global__ void negs_kernel(uint32_t* __restrict__ out, uint32_t* __restrict__ negwin,
                             const uint32_t* __restrict__ state, ShardGeo geo, uint64_t nsets,
                             uint32_t s, uint64_t seed, uint32_t epoch, int sampler, uint32_t W,
-                            uint32_t Re) {
+                            uint32_t Re, uint32_t walk_k, const uint32_t* __restrict__ wpos,
+                            const uint32_t* __restrict__ poff) {
   const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= nsets) return;
   const uint32_t G = geo.G, g = uint32_t(q % G);
   const uint64_t j = q / G;
   uint32_t win = 0;
   if (j < geo.nb[g]) {
+    // walk mode: the batch's walks were drawn first on the same stream
+    const uint64_t off = walk_k ? uint64_t(walk_k) * (wpos[poff[q + 1]] - wpos[poff[q]]) : 0;
+    const uint64_t s0 = G == 1 ? rng_keyed3(seed, kStreamSampling, epoch, j)
+                               : rng_keyed4(seed, kStreamSampling, epoch, j, g);
     for (uint32_t k = 0; k < s; ++k) {
       const uint32_t w = sampler == F2V_SAMPLER_PHILOX
                              ? philox_negative(seed, epoch, j, g, k, geo.n)
-                             : splitmix_negative(seed, epoch, j, g, G, k, geo.n);
+                             : uint32_t(rng_below(rng_draw(s0, off + k), geo.n));
       out[q * s + k] = w;
       const uint32_t bw = state[w] >> 1;
       if (bw < j && uint64_t(bw) + W >= j) win |= uint64_t(bw) + Re >= j ? 3u : 1u;
@@ -410,7 +415,8 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
   const ShardGeo geo = make_geo(c);
   negs_kernel<<<uint32_t((nsets + 255) / 256), 256, 0, c.stream>>>(
       c.negs_all.as<uint32_t>(), c.negwin.as<uint32_t>(), c.state.as<uint32_t>(), geo, nsets, s,
-      seed, epoch, sampler, W, Re);
+      seed, epoch, sampler, W, Re, c.walk_k, c.walk_k ? c.wpos.as<uint32_t>() : nullptr,
+      c.poff.as<uint32_t>());
   F2V_LAUNCHED(c.stream, "negs_kernel");
   if (c.nnz)
     window_scan_kernel<<<uint32_t((c.nnz + 255) / 256), 256, 0, c.stream>>>(

@@ -114,6 +114,12 @@ struct Ctx {
   void* peer_ctl[8] = {};
   void* peer_base[8][3] = {};  // IPC mappings to close
   uint64_t barriers = 0;
+  // walk mode (f2v_walk.cu): while walk_k > 0, rowptr/col/h_rowptr/nnz hold
+  // the per-epoch walk context and the graph CSR is parked here
+  uint32_t walk_k = 0;
+  DeviceBuf grow, gcol, wflag, wpos;
+  std::vector<uint64_t> h_growptr;
+  uint64_t gnnz = 0;
   DeviceBuf trace;  // DEBUG: per-position finalise timestamps (F2V_TRACE)
   DeviceBuf shufR, shufL;  // device Fisher-Yates (f2v_perm.cu)
 
@@ -140,6 +146,8 @@ void k_prepare_graph(Ctx& c);
 void k_shard_layout(Ctx& c, uint32_t batch, uint32_t G);
 void k_epoch_perm(Ctx& c, uint32_t epoch, uint64_t seed);
 void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sampler);
+void k_set_context(Ctx& c, uint32_t walk_k);   // f2v_walk.cu
+void k_epoch_walks(Ctx& c, uint32_t epoch, uint64_t seed);
 EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bool monitor);
 void k_epoch_restore(Ctx& c, uint64_t bad_step);
 void k_device_partition(Ctx& c, uint32_t n, uint64_t seed, uint32_t epoch, uint32_t* perm_out);

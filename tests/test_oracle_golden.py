@@ -266,3 +266,21 @@ def test_config1_trajectory_bit_exact(orc, sampler):
     assert np.array_equal(loss, g[f"{sampler}_loss"])
     assert np.array_equal(ctr, g[f"{sampler}_ctr"])
     assert sha(z) == str(g[f"{sampler}_z_sha"])
+
+
+@pytest.mark.parametrize("k", [1, 4])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_walk_mode_train_bit_exact(orc, k, kind):
+    """Walk mode (SampleMode::walk(k), sampling.cpp:27-61): the oracle's walks
+    (dead-end restarts, isolated starts, walks drawn before the negatives on
+    the batch stream) reproduce the reference's ref_train_mode bit for bit."""
+    ref = golden("walk.npz")
+    rc, z, losses, ctr, _ = orc.orc_train(ref["rowptr"], ref["col"], ref["z0"], 64, 5, 0.02, 2,
+                                          kind, 5, walk=k, threads=2)
+    assert rc == 0
+    assert np.array_equal(z, ref[f"train_k{k}_kind{kind}_z"])
+    assert np.array_equal(losses, ref[f"train_k{k}_kind{kind}_loss"])
+    assert np.array_equal(ctr, ref[f"train_k{k}_kind{kind}_ctr"])
+    # work counters (acceptance.cpp:263-266): every non-isolated vertex walks k steps
+    nonisolated = int((np.diff(ref["rowptr"]) > 0).sum())
+    assert int(ctr[0]) == 2 * k * nonisolated and int(ctr[1]) == 2 * 300 * 5
