@@ -133,6 +133,30 @@ __global__ void emit_kernel(const uint32_t* __restrict__ P, const uint32_t* __re
   (void)cnt;
 }
 
+// E items with the vertex, its chunk slots and the chunk's arc range resolved
+__global__ void emit_e_kernel(const uint32_t* __restrict__ P, const uint32_t* __restrict__ perm,
+                              const uint32_t* __restrict__ cbase,
+                              const uint64_t* __restrict__ rowptr, ep::EItem* __restrict__ items,
+                              uint32_t n, uint32_t C) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t o = P[p], m = P[p + 1] - o;
+  if (!m) return;
+  const uint32_t u = perm[p], cb = cbase[u], nch = cbase[u + 1] - cb;
+  const uint64_t r0 = rowptr[u], r1 = rowptr[u + 1];
+  for (uint32_t c = 0; c < m; ++c) {
+    ep::EItem it;
+    it.p = p;
+    it.u = u;
+    it.cb = cb;
+    it.c = c;
+    it.e0 = r0 + uint64_t(c) * C;
+    it.cnt = uint32_t(min(uint64_t(C), r1 - it.e0));
+    it.nch = nch;
+    items[o + c] = it;
+  }
+}
+
 // engine positions (batch-major) and each engine vertex's slot in its batch
 __global__ void engine_emit_kernel(const uint32_t* __restrict__ ecum,
                                    const uint32_t* __restrict__ nEng,
@@ -381,7 +405,7 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
   c.EP.ensure(sizeof(uint32_t) * (n + 1));
   c.LP.ensure(sizeof(uint32_t) * (n + 1));
   c.needs.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
-  c.items.ensure(sizeof(uint2) * std::max<uint64_t>(c.chunks, 1));
+  c.items.ensure(sizeof(ep::EItem) * std::max<uint64_t>(c.chunks, 1));
   c.litems.ensure(sizeof(uint2) * std::max<uint64_t>(c.lgroups, 1));
   c.negs_all.ensure(sizeof(uint32_t) * std::max<uint64_t>(nsets * s, 1));
   c.negwin.ensure(sizeof(uint32_t) * std::max<uint64_t>(nsets, 1));
@@ -436,9 +460,10 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
                                          c.EP.as<uint32_t>(), n + 1, c.stream));
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.nL.as<uint32_t>(),
                                          c.LP.as<uint32_t>(), n + 1, c.stream));
-  emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.EP.as<uint32_t>(), c.nE.as<uint32_t>(),
-                                                     c.items.as<uint2>(), n);
-  F2V_LAUNCHED(c.stream, "emit_kernel");
+  emit_e_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(
+      c.EP.as<uint32_t>(), c.perm.as<uint32_t>(), c.cbase.as<uint32_t>(),
+      c.rowptr.as<uint64_t>(), c.items.as<ep::EItem>(), n, c.tune.chunk);
+  F2V_LAUNCHED(c.stream, "emit_e_kernel");
   emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.LP.as<uint32_t>(), c.nL.as<uint32_t>(),
                                                      c.litems.as<uint2>(), n);
   F2V_LAUNCHED(c.stream, "emit_kernel");
@@ -492,7 +517,7 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   a.state = c.state.as<uint32_t>();
   a.negs = c.negs_all.as<uint32_t>();
   a.negwin = c.negwin.as<uint32_t>();
-  a.eitems = c.items.as<uint2>();
+  a.eitems = c.items.as<ep::EItem>();
   a.litems = c.litems.as<uint2>();
   a.n_eitems = uint32_t(c.chunks);
   a.n_eitems_dev = ctr + 9;

@@ -34,6 +34,14 @@ constexpr int kRefs = 32;       // engine: ring refs per vertex (+1 count word);
 constexpr int kRefStride = 36;  // words per vertex ref area (16-byte multiple for cp.async)
 constexpr int kMaxShards = 8;   // vertex shards (GPUs) of one run
 
+// An E work item with its vertex already resolved by the prep (emit_e_kernel),
+// so a warp's first dependent load is the chunk's column indices.
+struct alignas(16) EItem {
+  uint32_t p, u, cb, c;  // position, vertex, first chunk slot of u, chunk of u
+  uint64_t e0;           // first arc of the chunk
+  uint32_t cnt, nch;     // arcs in the chunk, chunks of u
+};
+
 struct EpochArgs {
   const uint64_t* rowptr;
   const uint32_t* col;
@@ -43,7 +51,7 @@ struct EpochArgs {
   uint32_t* state;
   const uint32_t* negs;
   const uint32_t* negwin;
-  const uint2* eitems;
+  const EItem* eitems;
   const uint2* litems;
   uint32_t n_eitems;                 // host upper bound (grid sizing)
   const uint32_t* n_eitems_dev;      // device count (written by the prep)
@@ -216,20 +224,16 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_
 }
 
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
-__device__ void do_E(const EpochArgs& a, uint32_t p, uint32_t c, int lane, uint32_t* qbuf) {
+__device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* qbuf) {
   using L = Lay<K, VEC>;
-  DCHECK(p < a.n, "E p=%u n=%u", p, a.n);
-  const uint32_t u = a.perm[p];
-  DCHECK(u < a.n, "E u=%u", u);
+  const uint32_t p = item.p, u = item.u, cb = item.cb, c = item.c, nch = item.nch;
+  DCHECK(p < a.n && u < a.n, "E p=%u u=%u n=%u", p, u, a.n);
   const uint32_t j = __ldg(a.state + u) >> 1;
-  const uint64_t r0 = a.rowptr[u], r1 = a.rowptr[u + 1];
-  const uint32_t cb = a.cbase[u];
-  const uint32_t nch = a.cbase[u + 1] - cb;
   const uint32_t cs = cb + c;
   DCHECK(c < nch && cs < a.chunks, "E c=%u nch=%u cs=%u chunks=%llu", c, nch, cs,
          (unsigned long long)a.chunks);
-  const uint64_t e0 = r0 + uint64_t(c) * a.C;
-  const uint64_t e1 = umin64(e0 + a.C, r1);
+  const uint64_t e0 = item.e0;
+  const uint64_t e1 = e0 + item.cnt;
   float zu[K];
   L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
   double acc[K];
@@ -520,7 +524,6 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) epoch_kernel(EpochArgs a) {
   const bool lrole = w >= kWarps - int(a.lwarps);
   uint32_t* counter = a.next + (lrole ? 1 : 0);
   const uint32_t total = lrole ? *a.n_litems : *a.n_eitems_dev;
-  const uint2* items = lrole ? a.litems : a.eitems;
   uint32_t it = 0;
   if (lane == 0) it = atomicAdd(counter, 1u);
   it = __shfl_sync(kFull, it, 0);
@@ -528,9 +531,12 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) epoch_kernel(EpochArgs a) {
     DCHECK(it < (lrole ? a.chunks + a.lslots + a.n : a.chunks), "item %u", it);
     uint32_t nxt = 0;
     if (lane == 0) nxt = atomicAdd(counter, 1u);  // claim ahead: hides the atomic's latency
-    const uint2 item = items[it];
-    if (lrole) do_L<KIND, K, VEC, MON, FAST>(a, item.x, item.y, lane, qbuf, rbuf);
-    else do_E<KIND, K, VEC, MON, FAST>(a, item.x, item.y, lane, qbuf);
+    if (lrole) {
+      const uint2 item = a.litems[it];
+      do_L<KIND, K, VEC, MON, FAST>(a, item.x, item.y, lane, qbuf, rbuf);
+    } else {
+      do_E<KIND, K, VEC, MON, FAST>(a, a.eitems[it], lane, qbuf);
+    }
     it = __shfl_sync(kFull, nxt, 0);
   }
 }
