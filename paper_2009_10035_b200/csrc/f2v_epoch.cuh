@@ -801,6 +801,7 @@ void launch_kind(Ctx& c, const EpochArgs& a, bool mon) {
 void launch_fast_k4(Ctx& c, const EpochArgs& a, bool mon);
 void launch_fast_k2(Ctx& c, const EpochArgs& a, bool mon);
 void launch_fast_k8(Ctx& c, const EpochArgs& a, bool mon);
+void launch_fast_lowd(Ctx& c, const EpochArgs& a, bool mon);
 void launch_exact_vec_k1(Ctx& c, const EpochArgs& a, bool mon);
 void launch_exact_vec_k2(Ctx& c, const EpochArgs& a, bool mon);
 void launch_exact_vec_k4(Ctx& c, const EpochArgs& a, bool mon);
@@ -812,12 +813,14 @@ void launch_exact_any_k8(Ctx& c, const EpochArgs& a, bool mon);
 void launch_exact_any_k16(Ctx& c, const EpochArgs& a, bool mon);
 void launch_exact_any_k32(Ctx& c, const EpochArgs& a, bool mon);
 
-// d = 64/128/256 run FAST when asked; everything else runs EXACT.
+// d = 64/128/256 and d <= 4 (lane-per-pair, rows_lowd) run FAST when asked;
+// everything else runs EXACT.
 inline void launch_epoch(Ctx& c, const EpochArgs& a, bool mon, bool fast) {
   const uint32_t d = a.d;
   if (fast && d == 128) launch_fast_k4(c, a, mon);
   else if (fast && d == 64) launch_fast_k2(c, a, mon);
   else if (fast && d == 256) launch_fast_k8(c, a, mon);
+  else if (fast && d <= uint32_t(kLowD)) launch_fast_lowd(c, a, mon);
   else if (d == 128) launch_exact_vec_k4(c, a, mon);
   else if (d == 64) launch_exact_vec_k2(c, a, mon);
   else if (d == 256) launch_exact_vec_k8(c, a, mon);

@@ -551,6 +551,76 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
   }
 }
 
+// ------------------------------------------------------- FAST low-d
+// d <= kLowD (the 2-D layout config): rows are too narrow to fill a warp, so
+// each lane owns one PAIR of the call -- its row (d floats) is one 8/16-byte
+// load, the dot / distance and the force term are lane-local fp32 -- and the
+// warp sums the d contribution columns of up to 32 pairs with a butterfly,
+// flushed into the fp64 accumulators (lane c owns column c, the masked
+// layout Lay<1, false>).  Same FAST numerics as rows_fast: fp32 pair math,
+// fp32 block sums, fp64 accumulation.
+constexpr int kLowD = 4;
+
+template <int KIND, bool MON, bool ATT>
+__device__ __forceinline__ void rows_lowd(const ForceParams& fp, uint32_t packed, int cnt,
+                                          int lane, uint32_t d, const float* __restrict__ zold,
+                                          const float* __restrict__ znew, const float (&zu1)[1],
+                                          double (&acc1)[1], double& lsum) {
+  constexpr bool SIG = KIND == F2V_SIGMOID;
+  float zu[kLowD];
+#pragma unroll
+  for (int c = 0; c < kLowD; ++c) zu[c] = __shfl_sync(kFull, zu1[0], c);  // lane c = column c
+  const bool mine = lane < cnt;
+  const uint32_t pk = packed;
+  const float* row = ((pk & kNewBit) ? znew : zold) + size_t(pk & ~kNewBit) * d;
+  float w[kLowD];
+  auto load = [&]() {
+#pragma unroll
+    for (int c = 0; c < kLowD; ++c)
+      w[c] = (mine && c < int(d)) ? ((pk & kNewBit) ? __ldcg(row + c) : __ldg(row + c)) : 0.0f;
+  };
+  load();
+  // Znew rows not yet final: re-load until no lane sees the sentinel
+  auto pending = [&]() {
+    bool b = false;
+#pragma unroll
+    for (int c = 0; c < kLowD; ++c) b |= __float_as_uint(w[c]) == kSentinel;
+    return b && mine && (pk & kNewBit);
+  };
+  uint32_t it = 0;
+  while (__any_sync(kFull, pending())) {
+    __nanosleep(20);
+    if (pending()) load();
+    if (++it == (1u << 28)) __trap();
+  }
+  float red = 0.f, nrm = 0.f;
+#pragma unroll
+  for (int c = 0; c < kLowD; ++c) {
+    if (SIG) {
+      red = fmaf(zu[c], w[c], red);
+      if (!ATT) nrm = fmaf(w[c], w[c], nrm);
+    } else {
+      w[c] = zu[c] - w[c];
+      red = fmaf(w[c], w[c], red);
+    }
+  }
+  const FastTerm t = fast_term<KIND, ATT, MON>(fp, red, nrm);
+  if (MON && mine) lsum = __dadd_rn(lsum, double(t.loss));
+  float col[kLowD];
+#pragma unroll
+  for (int c = 0; c < kLowD; ++c) col[c] = mine ? t.q * w[c] : 0.f;
+  if (!SIG && mine) col[0] += t.fb;
+#pragma unroll
+  for (int m = 16; m; m >>= 1)
+#pragma unroll
+    for (int c = 0; c < kLowD; ++c) col[c] += __shfl_xor_sync(kFull, col[c], m);
+  float mycol = 0.f;
+#pragma unroll
+  for (int c = 0; c < kLowD; ++c)
+    if (lane == c) mycol = col[c];
+  if (lane < int(d)) acc1[0] = __dadd_rn(acc1[0], double(mycol));
+}
+
 // The row-accumulation policy the epoch kernel is instantiated with.
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
 struct Rows {
@@ -560,7 +630,9 @@ struct Rows {
                                              const float* znew, const float (&zu)[K],
                                              double (&acc)[K], double& lsum,
                                              const float* ring = nullptr) {
-    if constexpr (FAST)
+    if constexpr (FAST && K == 1 && !VEC)
+      rows_lowd<KIND, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
+    else if constexpr (FAST)
       rows_fast<KIND, K, MON, ATT, RING>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum,
                                          ring);
     else

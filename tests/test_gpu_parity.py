@@ -345,7 +345,8 @@ def test_batch_clamp_and_tiny_graphs(f2v, orc, dev):
                                            "tdist", 3)
         assert rc == 0
         z_parity(z, zr)
-        np.testing.assert_allclose(losses, lr_, rtol=1e-9)
+        # d = 4 runs the FAST lane-per-pair path (fp32 pair math)
+        np.testing.assert_allclose(losses, lr_, rtol=LOSS_RTOL[cfg.precision])
         assert [ctr.attractive_evals, ctr.repulsive_evals] == list(cr)
 
 
@@ -457,3 +458,25 @@ def test_occupancy_builds_bitwise_identical(f2v, orc):
         dev.close()
     for l, z in outs[1:]:
         assert l == outs[0][0] and np.array_equal(z, outs[0][1])
+
+
+def test_config4_shape_low_d(f2v, orc, dev):
+    """Config 4's shape at reduced n: a random geometric graph in the unit
+    square, d = 2, t-dist -- the FAST lane-per-pair low-d path (rows_lowd)
+    -- epoch by epoch against the oracle."""
+    g = f2v.rgg_graph(20000, 12.0, 3)
+    n = g.num_vertices()
+    z0 = np.zeros((n, 2), np.float32)
+    orc.oracle().orc_random_embedding(n, 2, 1, z0)
+    cfg = f2v.TrainConfig(dim=2, batch=256, negatives=5, lr=0.02, epochs=20,
+                          model=kind_model(f2v, "tdist"), seed=1, monitor_loss=True,
+                          sampler="philox")
+    zref = z0.copy()
+    for e in range(2):
+        z, losses, ctr = run_epochs(f2v, dev, g, zref, cfg, first=e, run=1)
+        zr, lref = oracle_epoch(orc, g.row_offsets, g.col_indices, zref, 256, 5, 0.02, e,
+                                "tdist", 1, "philox")
+        z_parity(z, zr)
+        assert losses[0] == pytest.approx(lref, rel=LOSS_RTOL["fast"])
+        assert [ctr.attractive_evals, ctr.repulsive_evals] == [g.num_edges(), n * 5]
+        zref = zr
