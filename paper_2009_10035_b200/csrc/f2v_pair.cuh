@@ -520,6 +520,7 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
                                           const float* ring = nullptr) {
   using L = Lay<K, true>;
   constexpr int NB = F2V_FAST_INFLIGHT;
+  d = 32 * K;  // VEC layout: a compile-time row stride
   for (int k0 = 0; k0 < cnt; k0 += NB) {
     float w[NB / 8][8][K];
     uint32_t pks[NB];
