@@ -142,9 +142,12 @@ def test_world1_sharded_device_ipc_path(f2v, orc):
     assert launches > 0
 
 
-def test_allgather_driver_on_device(f2v, orc):
-    """dist.train_allgather over the CUDA per-step operators (world-1 gloo
-    group): per-step grad + failure vote + apply + row exchange."""
+@pytest.mark.parametrize("backend", ["gloo", "nccl"])
+def test_allgather_driver_on_device(f2v, orc, backend):
+    """dist.train_allgather over the CUDA per-step operators (world-1 group;
+    NCCL = the reference-granularity all-gather baseline on GPUs): per-step
+    grad + failure vote + apply + row exchange."""
+    import torch
     import torch.distributed as dist
 
     from paper_2009_10035_b200.dist import DeviceBackend, train_allgather
@@ -154,7 +157,10 @@ def test_allgather_driver_on_device(f2v, orc):
     port = s.getsockname()[1]
     s.close()
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=0, world_size=1)
+    if backend == "nccl":
+        torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=0, world_size=1)
+    tdev = torch.device("cuda", 0) if backend == "nccl" else None
     try:
         g = _graph(f2v, orc, 900, 2)
         n = g.num_vertices()
@@ -166,7 +172,7 @@ def test_allgather_driver_on_device(f2v, orc):
         with f2v.Device(0) as dv:
             dv.upload_graph(g)
             dv.set_embedding(z0)
-            losses = train_allgather(DeviceBackend(dv), n, cfg, 0, 1)
+            losses = train_allgather(DeviceBackend(dv), n, cfg, 0, 1, tensor_device=tdev)
             z = dv.get_embedding()
             rows = dv.get_rows(np.array([3, 1, 3], np.uint32))
             assert np.array_equal(rows, z[[3, 1, 3]])
