@@ -505,10 +505,6 @@ __device__ __forceinline__ void fast_block(const ForceParams& fp, int k0, int cn
   for (int k = 0; k < K; ++k) acc[k] = __dadd_rn(acc[k], double(a32[k]));
 }
 
-#ifndef F2V_L2_PREFETCH
-#define F2V_L2_PREFETCH 1
-#endif
-
 #ifndef F2V_FAST_INFLIGHT
 #define F2V_FAST_INFLIGHT 8  // row gathers in flight per warp (8; 16 measured slower)
 #endif
@@ -525,19 +521,6 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
   using L = Lay<K, true>;
   constexpr int NB = F2V_FAST_INFLIGHT;
   d = 32 * K;  // VEC layout: a compile-time row stride
-#if F2V_L2_PREFETCH
-  // lane l prefetches row l of the call into L2 (4 x 128-byte lines): all of
-  // the call's rows are in flight at once without holding registers, and the
-  // 8-row blocks below hit L2 (the coherence point, so Znew sentinels are
-  // still observed correctly)
-  if (cnt > 8 && lane < cnt && !(RING && (packed & kRingBit))) {
-    const char* row = reinterpret_cast<const char*>(((packed & kNewBit) ? znew : zold) +
-                                                    size_t(packed & ~kNewBit) * (32 * K));
-#pragma unroll
-    for (int q = 0; q < K; ++q)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(row + 128 * q));
-  }
-#endif
   for (int k0 = 0; k0 < cnt; k0 += NB) {
     float w[NB / 8][8][K];
     uint32_t pks[NB];
