@@ -1,8 +1,8 @@
 """DEBUG: C1 trajectory, per-epoch comparison vs the oracle (engine on/off)."""
 import os, sys
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle"))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
 import paper_2009_10035_b200 as f2v
 import pyoracle as orc
 g = f2v.sbm_graph(4096, 8, 0.03, 0.001, 4096)

@@ -1,8 +1,8 @@
 """DEBUG repro: hub-split epoch with a tiny chunk (F2V_CHUNK)."""
 import os, sys
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "oracle"))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
 import paper_2009_10035_b200 as f2v
 import pyoracle as orc
 prec = sys.argv[1] if len(sys.argv) > 1 else "fast"

@@ -1,7 +1,7 @@
 """DEBUG: per-batch completion profile of one C2 epoch (F2V_TRACE=1)."""
 import ctypes as C, os, sys, json
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["F2V_TRACE"] = "1"
 import paper_2009_10035_b200 as f2v
 lib = f2v._lib
