@@ -278,7 +278,8 @@ void f2v_destroy(f2v_ctx* h) {
         &c.state, &c.negs_all, &c.negwin, &c.items, &c.litems, &c.nE, &c.nL, &c.EP, &c.LP,
         &c.wtot, &c.needs, &c.scan_tmp, &c.epart, &c.eloss, &c.wcnt, &c.wl, &c.lpart, &c.lloss,
         &c.ploss, &c.counters, &c.trace, &c.shufR, &c.shufL, &c.nEng, &c.ecum, &c.epos,
-        &c.eslot, &c.eidx, &c.rcnt, &c.poff, &c.lperm, &c.grow, &c.gcol, &c.wflag, &c.wpos})
+        &c.eslot, &c.eidx, &c.rcnt, &c.poff, &c.lperm, &c.grow, &c.gcol, &c.wflag, &c.wpos,
+        &c.pcnt, &c.pslot})
     b->release();
   for (uint32_t g = 0; g < 8; ++g)  // peers' replicas mapped by f2v_shard_attach
     for (int i = 0; i < 3; ++i)

@@ -103,14 +103,17 @@ __global__ void src_kernel(const uint64_t* __restrict__ rowptr, uint32_t* __rest
 __global__ void needs_kernel(const uint32_t* __restrict__ perm, ShardGeo geo,
                              const uint32_t* __restrict__ state,
                              const uint32_t* __restrict__ wtot, const uint32_t* __restrict__ negwin,
-                             const uint32_t* __restrict__ lbase, uint32_t* __restrict__ needs,
-                             uint32_t* __restrict__ nL, uint32_t* __restrict__ nEng, int nodep) {
+                             const uint32_t* __restrict__ lbase,
+                             const uint32_t* __restrict__ cbase, uint32_t* __restrict__ needs,
+                             uint32_t* __restrict__ nL, uint32_t* __restrict__ nEng,
+                             uint32_t* __restrict__ pcnt, int nodep) {
   const uint32_t n = geo.n;
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > n) return;
   if (p == n) {
     nL[n] = 0;
     nEng[n] = 0;
+    pcnt[n] = 0;
     return;
   }
   const uint32_t u = perm[p];
@@ -122,6 +125,10 @@ __global__ void needs_kernel(const uint32_t* __restrict__ perm, ShardGeo geo,
   const bool own = u >= geo.rank_lo && u < geo.rank_hi;
   nL[p] = nd && own ? lbase[u + 1] - lbase[u] : 0u;
   nEng[p] = (nd & 2u) ? 1u : 0u;
+  // fp64 partial rows: one per chunk of a split row, one for the E total of a
+  // needs-L vertex, none otherwise (sized per epoch: C5-scale graphs fit)
+  const uint32_t nch = cbase[u + 1] - cbase[u];
+  pcnt[p] = own ? (nch > 1 ? nch : (nd ? 1u : 0u)) : 0u;
 }
 
 __global__ void emit_kernel(const uint32_t* __restrict__ P, const uint32_t* __restrict__ cnt,
@@ -161,13 +168,14 @@ __global__ void emit_e_kernel(const uint32_t* __restrict__ P, const uint32_t* __
 __global__ void engine_emit_kernel(const uint32_t* __restrict__ ecum,
                                    const uint32_t* __restrict__ nEng,
                                    const uint32_t* __restrict__ perm,
-                                   const uint32_t* __restrict__ cbase, uint4* __restrict__ erec,
+                                   const uint32_t* __restrict__ cbase,
+                                   const uint32_t* __restrict__ pslot, uint4* __restrict__ erec,
                                    uint32_t* __restrict__ eslot, uint32_t* __restrict__ eidx,
                                    uint32_t n, uint32_t b) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n || !nEng[p]) return;
   const uint32_t u = perm[p], i = ecum[p];
-  erec[i] = make_uint4(u, cbase[u], p, 0u);
+  erec[i] = make_uint4(u, cbase[u], p, pslot[p]);
   eslot[u] = i - ecum[uint64_t(p / b) * b];
   eidx[u] = i;
 }
@@ -409,7 +417,8 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
   c.litems.ensure(sizeof(uint2) * std::max<uint64_t>(c.lgroups, 1));
   c.negs_all.ensure(sizeof(uint32_t) * std::max<uint64_t>(nsets * s, 1));
   c.negwin.ensure(sizeof(uint32_t) * std::max<uint64_t>(nsets, 1));
-  c.epart.ensure(sizeof(double) * std::max<uint64_t>(c.chunks * c.d, 1));
+  c.pcnt.ensure(sizeof(uint32_t) * (size_t(n) + 1));
+  c.pslot.ensure(sizeof(uint32_t) * (size_t(n) + 1));
   c.eloss.ensure(sizeof(double) * std::max<uint64_t>(c.chunks, 1));
   c.wcnt.ensure(sizeof(uint32_t) * std::max<uint64_t>(c.chunks, 1));
   c.wl.ensure(sizeof(uint32_t) * std::max<uint64_t>(c.nnz, 1));
@@ -449,8 +458,9 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
   F2V_LAUNCHED(c.stream, "window_scan_kernel");
   needs_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
       c.perm.as<uint32_t>(), geo, c.state.as<uint32_t>(), c.wtot.as<uint32_t>(),
-      c.negwin.as<uint32_t>(), c.lbase.as<uint32_t>(), c.needs.as<uint32_t>(),
-      c.nL.as<uint32_t>(), c.nEng.as<uint32_t>(), std::getenv("F2V_DEBUG_NODEP") ? 1 : 0);
+      c.negwin.as<uint32_t>(), c.lbase.as<uint32_t>(), c.cbase.as<uint32_t>(),
+      c.needs.as<uint32_t>(), c.nL.as<uint32_t>(), c.nEng.as<uint32_t>(), c.pcnt.as<uint32_t>(),
+      std::getenv("F2V_DEBUG_NODEP") ? 1 : 0);
   F2V_LAUNCHED(c.stream, "needs_kernel");
   size_t tmp = 0;
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.nE.as<uint32_t>(), c.EP.as<uint32_t>(),
@@ -460,6 +470,27 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
                                          c.EP.as<uint32_t>(), n + 1, c.stream));
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.nL.as<uint32_t>(),
                                          c.LP.as<uint32_t>(), n + 1, c.stream));
+  F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.pcnt.as<uint32_t>(),
+                                         c.pslot.as<uint32_t>(), n + 1, c.stream));
+  {  // the epoch's partial rows (grow-only).  Every vertex needs at most its
+     // chunk count, so `chunks` rows always suffice: allocated once when that
+     // is small next to device memory; otherwise (C5-scale graphs) sized to
+     // this epoch's exact count, which costs one host sync per epoch.
+    const uint64_t bound = sizeof(double) * std::max<uint64_t>(c.chunks * c.d, 1);
+    size_t free_b = 0, total_b = 0;
+    if (c.epart.bytes < bound) F2V_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    (void)free_b;
+    const bool exact = std::getenv("F2V_EPART_EXACT") != nullptr;  // test hook
+    if (!exact && (c.epart.bytes >= bound || bound <= total_b / 8)) {
+      c.epart.ensure(bound);
+    } else {
+      uint32_t slots = 0;
+      F2V_CUDA(cudaMemcpyAsync(&slots, c.pslot.as<uint32_t>() + n, sizeof(slots),
+                               cudaMemcpyDeviceToHost, c.stream));
+      F2V_CUDA(cudaStreamSynchronize(c.stream));
+      c.epart.ensure(sizeof(double) * std::max<uint64_t>(uint64_t(slots) * c.d, 1));
+    }
+  }
   emit_e_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(
       c.EP.as<uint32_t>(), c.perm.as<uint32_t>(), c.cbase.as<uint32_t>(),
       c.rowptr.as<uint64_t>(), c.items.as<ep::EItem>(), n, c.tune.chunk);
@@ -472,7 +503,8 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
                                            c.ecum.as<uint32_t>(), n + 1, c.stream));
     engine_emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(
         c.ecum.as<uint32_t>(), c.nEng.as<uint32_t>(), c.perm.as<uint32_t>(),
-        c.cbase.as<uint32_t>(), c.epos.as<uint4>(), c.eslot.as<uint32_t>(),
+        c.cbase.as<uint32_t>(), c.pslot.as<uint32_t>(), c.epos.as<uint4>(),
+        c.eslot.as<uint32_t>(),
         c.eidx.as<uint32_t>(), n, c.sh_bs[0]);
     F2V_LAUNCHED(c.stream, "engine_emit_kernel");
   }
@@ -528,6 +560,7 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   a.lpo = c.lpo.as<uint32_t>();
   a.needs = c.needs.as<uint32_t>();
   a.epart = c.epart.as<double>();
+  a.pslot = c.pslot.as<uint32_t>();
   a.eloss = c.eloss.as<double>();
   a.wcnt = c.wcnt.as<uint32_t>();
   a.wl = c.wl.as<uint32_t>();

@@ -61,7 +61,8 @@ struct EpochArgs {
   const uint32_t* lbase;
   const uint32_t* lpo;
   const uint32_t* needs;  // per vertex: window arcs/negatives exist
-  double* epart;
+  double* epart;            // fp64 partial rows, compact: slots pslot[p] .. of position p
+  const uint32_t* pslot;    // per position: first partial slot (hub chunks / needs-L vertices)
   double* eloss;
   uint32_t* wcnt;
   uint32_t* wl;
@@ -230,6 +231,7 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   DCHECK(p < a.n && u < a.n, "E p=%u u=%u n=%u", p, u, a.n);
   const uint32_t j = __ldg(a.state + u) >> 1;
   const uint32_t cs = cb + c;
+  const uint32_t ps = __ldg(a.pslot + p);  // partial slots of u (used when nch > 1 or needs-L)
   DCHECK(c < nch && cs < a.chunks, "E c=%u nch=%u cs=%u chunks=%llu", c, nch, cs,
          (unsigned long long)a.chunks);
   const uint64_t e0 = item.e0;
@@ -276,7 +278,7 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
       do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
       finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
     } else {
-      L::store_acc(a.epart + size_t(cs) * a.d, lane, a.d, acc);
+      L::store_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);
       const double ls = MON ? warp_sum_d(lsum) : 0.0;
       if (lane == 0) {
         if (MON) __stcg(a.eloss + cs, ls);
@@ -289,7 +291,7 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
     return;
   }
   // hub chunk: publish the partial; the last E arrival combines in chunk order
-  L::store_acc(a.epart + size_t(cs) * a.d, lane, a.d, acc);
+  L::store_acc(a.epart + size_t(ps + c) * a.d, lane, a.d, acc);
   {
     const double ls = MON ? warp_sum_d(lsum) : 0.0;
     if (lane == 0) {
@@ -303,11 +305,11 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   if (lane == 0) last = atomicAdd(a.ecnt + u, 1u) == nch - 1 ? 1u : 0u;
   if (!__shfl_sync(kFull, last, 0)) return;
   __threadfence();
-  L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
+  L::load_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);
   lsum = (MON && lane == 0) ? __ldcg(a.eloss + cb) : 0.0;
 #pragma unroll 4
   for (uint32_t qq = 1; qq < nch; ++qq) {
-    L::add_acc(a.epart + size_t(cb + qq) * a.d, lane, a.d, acc);
+    L::add_acc(a.epart + size_t(ps + qq) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __dadd_rn(lsum, __ldcg(a.eloss + cb + qq));
   }
   if (lane == 0) a.ecnt[u] = 0;
@@ -315,7 +317,7 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
     do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
     finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
   } else {
-    L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);  // the E total
+    L::store_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);  // the E total
     if (MON && lane == 0) __stcg(a.eloss + cb, lsum);  // lane 0 holds the whole sum here
     __threadfence();
     __syncwarp();
@@ -450,17 +452,18 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   }
   if (lt && lane == 0) lt[1] = globaltimer();
   const uint32_t c0 = cl * a.G, c1 = umin32(nch, c0 + a.G);
+  const uint32_t ps = __ldg(a.pslot + p);  // the E total of u lives in partial slot ps
   const uint32_t nflag = a.needs[u];
   const bool eng = (nflag & 2u) != 0;  // the chain engine finalises u (one-L-item vertices)
   if (nchL == 1) {
-    L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
+    L::load_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __ldcg(a.eloss + cb);
     int nr = 0;
     if (eng) {  // E total + window arcs except ring refs + negatives -> pre-final P(u)
       window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
                                               lsum, true);
       do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
-      L::store_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
+      L::store_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);
       const double ls = MON ? warp_sum_d(lsum) : 0.0;
       if (lane == 0) {
         if (MON) __stcg(a.eloss + cb, ls);
@@ -499,7 +502,7 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   if (lane == 0) last = atomicAdd(a.lcnt + u, 1u) == nchL - 1 ? 1u : 0u;
   if (!__shfl_sync(kFull, last, 0)) return;
   __threadfence();
-  L::load_acc(a.epart + size_t(cb) * a.d, lane, a.d, acc);
+  L::load_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);
   lsum = (MON && lane == 0) ? __ldcg(a.eloss + cb) : 0.0;
   const uint32_t lp = a.lpo[u];
 #pragma unroll 4
@@ -608,7 +611,8 @@ __global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs 
       const uint32_t i = e0 + w + uint32_t(kk) * kEngineWarps;
       if (ok) {
         char* dst = reinterpret_cast<char*>(slotp(jj & 1, kk));
-        const char* P = reinterpret_cast<const char*>(a.epart + size_t(cb) * d);
+        const uint32_t psl = __shfl_sync(kFull, r.w, kk);
+        const char* P = reinterpret_cast<const char*>(a.epart + size_t(psl) * d);
         const char* Z = reinterpret_cast<const char*>(a.zold + size_t(u) * d);
         const char* R = reinterpret_cast<const char*>(a.rl + size_t(i) * kRefStride);
         for (uint32_t off = lane * 16; off < d * 8; off += 512) cp_async16(dst + off, P + off);
@@ -687,7 +691,7 @@ __global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs 
           ++waits;
           wait_ns += globaltimer() - t0;
         }
-        L::load_acc(a.epart + size_t(cb) * d, lane, d, acc);
+        L::load_acc(a.epart + size_t(rec.w) * d, lane, d, acc);
         L::load(a.zold + size_t(u) * d, lane, d, zu, false);
         const uint32_t* R = a.rl + size_t(i) * kRefStride;
         nrefs = __ldcg(R);

@@ -85,7 +85,7 @@ struct Ctx {
 
   // epoch buffers
   DeviceBuf perm, state, negs_all, negwin, items, litems, nE, nL, EP, LP, wtot, needs, scan_tmp,
-      epart, eloss, wcnt, wl, lpart, lloss, ploss, counters;
+      epart, eloss, wcnt, wl, lpart, lloss, ploss, counters, pcnt, pslot;
   uint32_t last_litems = 0;
   DeviceBuf nEng, ecum, epos, eslot, eidx, rcnt;  // chain engine lists
   cudaStream_t stream2 = nullptr;                 // the chain engine runs here

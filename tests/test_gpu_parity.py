@@ -480,3 +480,28 @@ def test_config4_shape_low_d(f2v, orc, dev):
         assert losses[0] == pytest.approx(lref, rel=LOSS_RTOL["fast"])
         assert [ctr.attractive_evals, ctr.repulsive_evals] == [g.num_edges(), n * 5]
         zref = zr
+
+
+def test_exact_partial_sizing_identical(f2v, orc):
+    """The compact per-epoch partial-row layout sized exactly (the path
+    C5-scale graphs take) gives the same epochs as the default sizing."""
+    g = f2v.rmat_graph(13, 16, seed=5)  # hubs split across chunks
+    n = g.num_vertices()
+    z0 = np.zeros((n, 128), np.float32)
+    orc.oracle().orc_random_embedding(n, 128, 3, z0)
+    cfg = f2v.TrainConfig(dim=128, batch=256, negatives=5, lr=0.02, epochs=2,
+                          model=kind_model(f2v, "tdist"), seed=4, monitor_loss=True,
+                          sampler="philox")
+    outs = []
+    for exact in (False, True):
+        if exact:
+            os.environ["F2V_EPART_EXACT"] = "1"
+        try:
+            dev = f2v.Device(0)
+            dev.upload_graph(g)
+            dev.set_embedding(z0)
+            outs.append((dev.train_epochs(cfg), dev.get_embedding()))
+            dev.close()
+        finally:
+            os.environ.pop("F2V_EPART_EXACT", None)
+    assert outs[0][0] == outs[1][0] and np.array_equal(outs[0][1], outs[1][1])
