@@ -49,12 +49,15 @@ CONFIGS = {
     "c3": ("chung_lu", dict(n=3_000_000, exponent=2.2, min_deg=2.0, max_deg=30000.0,
                             mean_deg=78.0, seed=1), "sigmoid", 128, 384, 5, 0.02, 1),
     "c4": ("rgg", dict(n=1_000_000, mean_deg=12.0, seed=1), "tdist", 2, 256, 5, 0.02, 20),
+    "c5": ("rmat", dict(scale=26, edge_factor=16, a=0.57, b=0.19, c=0.19, seed=1), "sigmoid", 128,
+           512, 5, 0.02, 1),
 }
 WORKLOAD_NAMES = {
     "c1": "SBM n=4096 (8 blocks, p_in .03, p_out .001), sigmoid, d=128, b=256, s=5, lr .02",
     "c2": "R-MAT scale 20 (ef 16, .57/.19/.19/.05), t-dist, d=128, b=384, s=5, lr .02",
     "c3": "Chung-Lu n=3M power-law 2.2 (min 2, max 30000, mean 78), sigmoid, d=128, b=384, s=5",
     "c4": "RGG n=1M unit square (mean degree 12), t-dist, d=2, b=256, s=5, lr .02",
+    "c5": "R-MAT scale 26 (ef 16, .57/.19/.19/.05), sigmoid, d=128, b=512, s=5, lr .02",
 }
 
 
