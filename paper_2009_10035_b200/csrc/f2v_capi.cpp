@@ -256,9 +256,6 @@ f2v_ctx* f2v_create(int32_t device) {
     h->c.device = device;
     h->c.num_sms = prop.multiProcessorCount;
     F2V_CUDA(cudaStreamCreateWithFlags(&h->c.stream, cudaStreamNonBlocking));
-    F2V_CUDA(cudaStreamCreateWithFlags(&h->c.stream2, cudaStreamNonBlocking));
-    F2V_CUDA(cudaEventCreateWithFlags(&h->c.ev_prep, cudaEventDisableTiming));
-    F2V_CUDA(cudaEventCreateWithFlags(&h->c.ev_engine, cudaEventDisableTiming));
     load_tuning(h->c.tune);
   });
   if (rc != F2V_OK) {
@@ -277,8 +274,7 @@ void f2v_destroy(f2v_ctx* h) {
         &c.z[0], &c.z[1], &c.grads, &c.ids, &c.negs, &c.vloss, &c.bad, &c.scratch, &c.perm,
         &c.state, &c.negs_all, &c.negwin, &c.items, &c.litems, &c.nE, &c.nL, &c.EP, &c.LP,
         &c.wtot, &c.needs, &c.scan_tmp, &c.epart, &c.eloss, &c.wcnt, &c.wl, &c.lpart, &c.lloss,
-        &c.ploss, &c.counters, &c.trace, &c.shufR, &c.shufL, &c.nEng, &c.ecum, &c.epos,
-        &c.eslot, &c.eidx, &c.rcnt, &c.poff, &c.lperm, &c.grow, &c.gcol, &c.wflag, &c.wpos,
+        &c.ploss, &c.counters, &c.trace, &c.shufR, &c.shufL, &c.poff, &c.lperm, &c.grow, &c.gcol, &c.wflag, &c.wpos,
         &c.pcnt, &c.pslot})
     b->release();
   for (uint32_t g = 0; g < 8; ++g)  // peers' replicas mapped by f2v_shard_attach
@@ -288,9 +284,6 @@ void f2v_destroy(f2v_ctx* h) {
   for (cudaEvent_t e : c.ev_kernel) cudaEventDestroy(e);
   if (c.ev_begin) cudaEventDestroy(c.ev_begin);
   if (c.ev_end) cudaEventDestroy(c.ev_end);
-  if (c.ev_prep) cudaEventDestroy(c.ev_prep);
-  if (c.ev_engine) cudaEventDestroy(c.ev_engine);
-  if (c.stream2) cudaStreamDestroy(c.stream2);
   if (c.stream) cudaStreamDestroy(c.stream);
   delete h;
 }

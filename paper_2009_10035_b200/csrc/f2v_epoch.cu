@@ -83,12 +83,12 @@ __global__ void scatter_kernel(const uint32_t* __restrict__ lperm, const uint32_
 __global__ void window_scan_kernel(const uint32_t* __restrict__ src,
                                    const uint32_t* __restrict__ col,
                                    const uint32_t* __restrict__ state, uint32_t* __restrict__ wtot,
-                                   uint64_t nnz, uint32_t W, uint32_t Re) {
+                                   uint64_t nnz, uint32_t W) {
   const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (e >= nnz) return;
   const uint32_t u = __ldg(src + e), v = __ldg(col + e);
   const uint32_t j = __ldg(state + u) >> 1, bv = __ldg(state + v) >> 1;
-  if (bv < j && bv + W >= j) atomicOr(wtot + u, bv + Re >= j ? 3u : 1u);  // bit1: engine-recent
+  if (bv < j && bv + W >= j) atomicOr(wtot + u, 1u);
 }
 
 // src[e] = the row of arc e (static per graph)
@@ -105,14 +105,13 @@ __global__ void needs_kernel(const uint32_t* __restrict__ perm, ShardGeo geo,
                              const uint32_t* __restrict__ wtot, const uint32_t* __restrict__ negwin,
                              const uint32_t* __restrict__ lbase,
                              const uint32_t* __restrict__ cbase, uint32_t* __restrict__ needs,
-                             uint32_t* __restrict__ nL, uint32_t* __restrict__ nEng,
+                             uint32_t* __restrict__ nL,
                              uint32_t* __restrict__ pcnt, int nodep) {
   const uint32_t n = geo.n;
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p > n) return;
   if (p == n) {
     nL[n] = 0;
-    nEng[n] = 0;
     pcnt[n] = 0;
     return;
   }
@@ -120,11 +119,9 @@ __global__ void needs_kernel(const uint32_t* __restrict__ perm, ShardGeo geo,
   const uint32_t j = state[u] >> 1;
   const uint32_t nw = negwin[geo.G == 1 ? j : j * geo.G + ep::shard_of(u, n, geo.G)];
   uint32_t nd = ((wtot[u] | nw) & 1u) && !nodep ? 1u : 0u;
-  if (nd && (wtot[u] & 2u) && lbase[u + 1] - lbase[u] == 1) nd |= 2u;  // the chain engine's
   needs[u] = nd;
   const bool own = u >= geo.rank_lo && u < geo.rank_hi;
   nL[p] = nd && own ? lbase[u + 1] - lbase[u] : 0u;
-  nEng[p] = (nd & 2u) ? 1u : 0u;
   // fp64 partial rows: one per chunk of a split row, one for the E total of a
   // needs-L vertex, none otherwise (sized per epoch: C5-scale graphs fit)
   const uint32_t nch = cbase[u + 1] - cbase[u];
@@ -164,28 +161,10 @@ __global__ void emit_e_kernel(const uint32_t* __restrict__ P, const uint32_t* __
   }
 }
 
-// engine positions (batch-major) and each engine vertex's slot in its batch
-__global__ void engine_emit_kernel(const uint32_t* __restrict__ ecum,
-                                   const uint32_t* __restrict__ nEng,
-                                   const uint32_t* __restrict__ perm,
-                                   const uint32_t* __restrict__ cbase,
-                                   const uint32_t* __restrict__ pslot, uint4* __restrict__ erec,
-                                   uint32_t* __restrict__ eslot, uint32_t* __restrict__ eidx,
-                                   uint32_t n, uint32_t b) {
-  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= n || !nEng[p]) return;
-  const uint32_t u = perm[p], i = ecum[p];
-  erec[i] = make_uint4(u, cbase[u], p, pslot[p]);
-  eslot[u] = i - ecum[uint64_t(p / b) * b];
-  eidx[u] = i;
-}
-
-// negatives of every (step, shard) set q = t G + g, and whether any of them is
-// a window row of step t (then its vertices need an L item)
 __global__ void negs_kernel(uint32_t* __restrict__ out, uint32_t* __restrict__ negwin,
                             const uint32_t* __restrict__ state, ShardGeo geo, uint64_t nsets,
                             uint32_t s, uint64_t seed, uint32_t epoch, int sampler, uint32_t W,
-                            uint32_t Re, uint32_t walk_k, const uint32_t* __restrict__ wpos,
+                            uint32_t walk_k, const uint32_t* __restrict__ wpos,
                             const uint32_t* __restrict__ poff) {
   const uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (q >= nsets) return;
@@ -203,7 +182,7 @@ __global__ void negs_kernel(uint32_t* __restrict__ out, uint32_t* __restrict__ n
                              : uint32_t(rng_below(rng_draw(s0, off + k), geo.n));
       out[q * s + k] = w;
       const uint32_t bw = state[w] >> 1;
-      if (bw < j && uint64_t(bw) + W >= j) win |= uint64_t(bw) + Re >= j ? 3u : 1u;
+      if (bw < j && uint64_t(bw) + W >= j) win = 1u;
     }
   }
   negwin[q] = win;
@@ -254,10 +233,8 @@ void load_tuning(EpochTuning& t) {
   t.recent = env_u32("F2V_RECENT", t.recent);
   t.lwarps = std::min(uint32_t(ep::kWarps - 1), std::max(1u, env_u32("F2V_LWARPS", t.lwarps)));
   if (const char* e = std::getenv("F2V_PRECISION")) t.fast = std::strcmp(e, "exact") != 0;
-  t.erecent = env_u32("F2V_ERECENT", t.erecent);
   t.ctas = env_u32("F2V_CTAS", t.ctas);
   t.minb = env_u32("F2V_MINB", t.minb);
-  if (t.erecent >= t.window) t.erecent = t.window - 1;
 }
 
 // Static per-graph chunk / L-group layout (depends on chunk and lgroup only).
@@ -427,39 +404,21 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
   c.ploss.ensure(sizeof(double) * std::max<uint32_t>(n, 1));
   c.counters.ensure(64);
   const uint32_t W = c.tune.window;
-  // effective engine window: 0 when the engine cannot run for this layout
-  uint32_t Re = c.tune.erecent;
-  {
-    const size_t stage = 2 * size_t(ep::kEngineWarps) * ep::kStage *
-                         ((size_t(c.d) * 12 + ep::kRefStride * 4 + 15) / 16 * 16);
-    const size_t budget = 210u * 1024u > stage ? 210u * 1024u - stage : 0;
-    c.eff_maxe = Re ? uint32_t(std::min<size_t>(64, budget / (size_t(Re + 1) * c.d * 4))) : 0u;
-    if (Re && (!c.tune.fast || c.eff_maxe < 4 || n >= kIdMask || c.shards != 1 ||
-               (c.d != 64 && c.d != 128 && c.d != 256)))
-      Re = 0;
-    c.eff_re = Re;
-  }
-  c.nEng.ensure(sizeof(uint32_t) * (n + 1));
-  c.ecum.ensure(sizeof(uint32_t) * (n + 1));
-  c.epos.ensure(sizeof(uint4) * std::max<uint32_t>(n, 1));
-  c.eslot.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
-  c.eidx.ensure(sizeof(uint32_t) * std::max<uint32_t>(n, 1));
-  c.rcnt.ensure(sizeof(uint32_t) * ep::kRefStride * std::max<uint32_t>(n, 1));
   const ShardGeo geo = make_geo(c);
   negs_kernel<<<uint32_t((nsets + 255) / 256), 256, 0, c.stream>>>(
       c.negs_all.as<uint32_t>(), c.negwin.as<uint32_t>(), c.state.as<uint32_t>(), geo, nsets, s,
-      seed, epoch, sampler, W, Re, c.walk_k, c.walk_k ? c.wpos.as<uint32_t>() : nullptr,
+      seed, epoch, sampler, W, c.walk_k, c.walk_k ? c.wpos.as<uint32_t>() : nullptr,
       c.poff.as<uint32_t>());
   F2V_LAUNCHED(c.stream, "negs_kernel");
   if (c.nnz)
     window_scan_kernel<<<uint32_t((c.nnz + 255) / 256), 256, 0, c.stream>>>(
         c.src.as<uint32_t>(), c.col.as<uint32_t>(), c.state.as<uint32_t>(),
-        c.wtot.as<uint32_t>(), c.nnz, W, Re);
+        c.wtot.as<uint32_t>(), c.nnz, W);
   F2V_LAUNCHED(c.stream, "window_scan_kernel");
   needs_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
       c.perm.as<uint32_t>(), geo, c.state.as<uint32_t>(), c.wtot.as<uint32_t>(),
       c.negwin.as<uint32_t>(), c.lbase.as<uint32_t>(), c.cbase.as<uint32_t>(),
-      c.needs.as<uint32_t>(), c.nL.as<uint32_t>(), c.nEng.as<uint32_t>(), c.pcnt.as<uint32_t>(),
+      c.needs.as<uint32_t>(), c.nL.as<uint32_t>(), c.pcnt.as<uint32_t>(),
       std::getenv("F2V_DEBUG_NODEP") ? 1 : 0);
   F2V_LAUNCHED(c.stream, "needs_kernel");
   size_t tmp = 0;
@@ -498,16 +457,6 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
   emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.LP.as<uint32_t>(), c.nL.as<uint32_t>(),
                                                      c.litems.as<uint2>(), n);
   F2V_LAUNCHED(c.stream, "emit_kernel");
-  if (Re) {
-    F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.nEng.as<uint32_t>(),
-                                           c.ecum.as<uint32_t>(), n + 1, c.stream));
-    engine_emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(
-        c.ecum.as<uint32_t>(), c.nEng.as<uint32_t>(), c.perm.as<uint32_t>(),
-        c.cbase.as<uint32_t>(), c.pslot.as<uint32_t>(), c.epos.as<uint4>(),
-        c.eslot.as<uint32_t>(),
-        c.eidx.as<uint32_t>(), n, c.sh_bs[0]);
-    F2V_LAUNCHED(c.stream, "engine_emit_kernel");
-  }
   // numbers of E and L items (device values, read back asynchronously with the run)
   F2V_CUDA(cudaMemcpyAsync(c.counters.as<uint32_t>() + 8, c.LP.as<uint32_t>() + n,
                            sizeof(uint32_t), cudaMemcpyDeviceToDevice, c.stream));
@@ -586,13 +535,6 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   if (multi)
     for (uint32_t g = 0; g < c.world; ++g)
       if (int32_t(g) != c.rank) a.peer_znew[a.npeers++] = c.peer_z[g][nxt];
-  a.rl = c.rcnt.as<uint32_t>();
-  a.erec = c.epos.as<uint4>();
-  a.ecum = c.ecum.as<uint32_t>();
-  a.eslot = c.eslot.as<uint32_t>();
-  a.eidx = c.eidx.as<uint32_t>();
-  a.Re = c.eff_re;  // decided by the prep (0: no engine this epoch)
-  a.maxe = c.eff_maxe;
   a.eta = eta;
   a.fp = fp;
   a.nodep = std::getenv("F2V_DEBUG_NODEP") ? 1 : 0;
@@ -601,13 +543,11 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   a.lslots = c.lslots;
   a.trace = nullptr;
   a.ltrace = nullptr;
-  a.etrace = nullptr;
   if (std::getenv("F2V_TRACE")) {
     const uint32_t nbt = c.steps;
     c.trace.ensure(sizeof(unsigned long long) * (5ull * std::max<uint32_t>(c.n, 1) + 3ull * nbt + 2));
     a.trace = c.trace.as<unsigned long long>();
     a.ltrace = a.trace + c.n;
-    a.etrace = a.ltrace + 4ull * c.n;
     F2V_CUDA(cudaMemsetAsync(a.ltrace, 0,
                              sizeof(unsigned long long) * (4ull * c.n + 3ull * nbt + 2), c.stream));
   }

@@ -30,8 +30,6 @@ constexpr int kWarps = 8;       // warps per CTA
 // (Ctx::occ_ms); results are identical.
 constexpr int kQ = 64;          // per-warp compaction queue (entries)
 constexpr int kRq = 64;         // per-warp parking lot for the most recent window arcs
-constexpr int kRefs = 32;       // engine: ring refs per vertex (+1 count word); more go global
-constexpr int kRefStride = 36;  // words per vertex ref area (16-byte multiple for cp.async)
 constexpr int kMaxShards = 8;   // vertex shards (GPUs) of one run
 
 // An E work item with its vertex already resolved by the prep (emit_e_kernel),
@@ -80,20 +78,12 @@ struct EpochArgs {
   // into the peers' Znew replicas (NVLink P2P) when npeers > 0
   uint32_t shards, npeers;
   float* peer_znew[kMaxShards];
-  uint32_t Re;              // chain engine: arcs of age <= Re to ring rows are its (0 = off)
-  uint32_t* rl;             // engine: per engine vertex [count, ring refs...] (kRefs words)
-  const uint4* erec;        // engine: per engine index {vertex, cbase, position, 0}
-  const uint32_t* ecum;     // engine: exclusive count of engine positions (n + 1)
-  const uint32_t* eslot;    // engine: per vertex index within its batch's engine list
-  const uint32_t* eidx;     // engine: per vertex global engine index
-  uint32_t maxe;            // engine: ring rows per batch
   float eta;
   ForceParams fp;
   uint64_t nnz, chunks, lslots;  // bounds, used by F2V_DEVICE_CHECKS builds
   int nodep;                    // DEBUG (F2V_DEBUG_NODEP): every row read from Zold, no waits
   unsigned long long* trace;    // DEBUG (F2V_TRACE): per position finalise time (ns)
   unsigned long long* ltrace;   // DEBUG (F2V_TRACE): per position L-item stage times (4 x ns)
-  unsigned long long* etrace;   // DEBUG (F2V_TRACE): engine per batch [start, computed, staged]
 };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
@@ -199,7 +189,7 @@ __device__ __noinline__ void store_peers(const EpochArgs& a, uint32_t u, int lan
 template <int K, bool VEC, bool MON>
 __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_t u, int lane,
                                          const float (&zu)[K], const double (&acc)[K],
-                                         double lsum, float* ring_row = nullptr) {
+                                         double lsum) {
   using L = Lay<K, VEC>;
   bool bad = false;
   float nz[K];
@@ -210,7 +200,6 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_
     nz[k] = __fsub_rn(zu[k], __fmul_rn(a.eta, g));
     if (nz[k] != nz[k]) nz[k] = __int_as_float(0x7fffffff);  // never the sentinel NaN
   }
-  if (ring_row) L::store_smem(ring_row, lane, a.d, nz);    // the chain engine's own copy
   L::store(a.znew + size_t(u) * a.d, lane, a.d, nz);  // publishes the row (sentinel-free)
   if (a.npeers) store_peers<K, VEC>(a, u, lane, nz);  // the peers' replicas, over NVLink
   const bool any_bad = __any_sync(kFull, bad);
@@ -354,9 +343,8 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, u
                                                uint32_t c0, uint32_t c1, int lane,
                                                uint32_t* qbuf, uint32_t* rbuf, int& nr,
                                                const float (&zu)[K], double (&acc)[K],
-                                               double& lsum, bool defer = false) {
+                                               double& lsum) {
   const uint64_t r0 = a.rowptr[u];
-  const uint64_t obase = r0 + uint64_t(c0) * a.C;  // engine mode: recent ids written here
   const uint32_t cb = a.cbase[u];
   RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0};
   for (uint32_t cc = c0; cc < c1; cc += 32) {
@@ -391,26 +379,10 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, u
         DCHECK(v < a.n, "L wl v=%u", v);
         st = ld_relaxed(a.state + v);
         const uint32_t age = j - (st >> 1);
-        if (defer) {  // engine mode: arcs to rows in the engine's ring are the engine's
-          recent = age <= a.Re && (__ldg(a.needs + v) & 2u) && __ldg(a.eslot + v) < a.maxe;
-          old = !recent;
-        } else {
-          old = age > a.R;
-          recent = !old;
-        }
+        old = age > a.R;
+        recent = !old;
       }
       const uint32_t rm = __ballot_sync(kFull, recent);
-      if (defer) {
-        // ring refs beyond kRefs are taken here, from the global copy of the row
-        const int rank = nr + __popc(rm & lanemask_lt(lane));
-        const bool keep = recent && rank < kRefs;
-        if (keep)
-          a.rl[size_t(a.eidx[u]) * kRefStride + 1 + rank] =
-              kRingBit | (((st >> 1) % (a.Re + 1)) * a.maxe + __ldg(a.eslot + v));
-        q.push(a, lane, old || (recent && !keep), v | kNewBit, zu, acc, lsum);
-        nr = min(kRefs, nr + __popc(rm));
-        continue;
-      }
       q.push(a, lane, old, v | kNewBit, zu, acc, lsum);
       // park the recent ones (processed in place if the parking lot is full)
       if (nr + __popc(rm) > kRq) {
@@ -453,28 +425,10 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   if (lt && lane == 0) lt[1] = globaltimer();
   const uint32_t c0 = cl * a.G, c1 = umin32(nch, c0 + a.G);
   const uint32_t ps = __ldg(a.pslot + p);  // the E total of u lives in partial slot ps
-  const uint32_t nflag = a.needs[u];
-  const bool eng = (nflag & 2u) != 0;  // the chain engine finalises u (one-L-item vertices)
   if (nchL == 1) {
     L::load_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __ldcg(a.eloss + cb);
     int nr = 0;
-    if (eng) {  // E total + window arcs except ring refs + negatives -> pre-final P(u)
-      window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
-                                              lsum, true);
-      do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
-      L::store_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);
-      const double ls = MON ? warp_sum_d(lsum) : 0.0;
-      if (lane == 0) {
-        if (MON) __stcg(a.eloss + cb, ls);
-        __stcg(a.rl + size_t(a.eidx[u]) * kRefStride, uint32_t(nr));
-      }
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) st_relaxed(a.vflag + u, 2u);
-      if (lt && lane == 0) lt[2] = globaltimer();
-      return;
-    }
     // E total + old window arcs + negatives + recent arcs
     window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
     do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
@@ -544,203 +498,6 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) epoch_kernel(EpochArgs a) {
   }
 }
 
-// The chain engine: ONE CTA that walks the batches
-// of the epoch in order and finalises the "engine vertices" (one-L-item
-// vertices with arcs to the last Re batches).  Their L items hand it a
-// pre-final partial P(u) (E total + every window arc except those into the
-// engine's ring + the negatives) and the ring references; rows it finalised in
-// the last Re batches stay in a shared-memory ring, so a batch-to-batch
-// dependency costs a __syncthreads and a shared load instead of global-memory
-// round trips.  P(u) and z_u of the next batch are staged into shared memory
-// with cp.async while the current batch computes.  Batch j's ring rows are
-// reused at batch j+Re+1.
-constexpr int kEngineWarps = 8;
-constexpr int kStage = 2;  // staged vertices per warp per batch (x2 buffers)
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const uint32_t sa = uint32_t(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait_group() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int KIND, int K, bool VEC, bool MON, bool FAST>
-__global__ void __launch_bounds__(kEngineWarps * 32, 2) engine_kernel(EpochArgs a) {
-  extern __shared__ float4 smem4[];
-  using L = Lay<K, VEC>;
-  const int lane = threadIdx.x & 31;
-  const int w = threadIdx.x >> 5;
-  const uint32_t d = a.d;
-  const uint32_t RS = a.Re + 1;
-  float* ring = reinterpret_cast<float*>(smem4);
-  // staging: per warp kStage slots of [P (d doubles) | z_u (d floats) | refs (kRefStride words)]
-  const size_t slot_words = (size_t(d) * 12 + kRefStride * 4 + 15) / 16 * 4;
-  uint32_t* stage = reinterpret_cast<uint32_t*>(ring + size_t(RS) * a.maxe * d) +
-                    size_t(w) * 2 * kStage * slot_words;  // two buffers per warp
-  // records of this warp's first kStage vertices, four batches in flight;
-  // staging is double-buffered and filled two batches ahead
-  __shared__ uint4 srec[4][kEngineWarps][kStage];
-  __shared__ uint32_t staged[2][kEngineWarps][kStage];
-  const uint32_t nb = (a.n + a.b - 1) / a.b;
-  auto cum = [&](uint32_t j) { return __ldg(a.ecum + umin64(uint64_t(j) * a.b, a.n)); };
-  auto slotp = [&](uint32_t buf, int k) {
-    return stage + (size_t(buf) * kStage + k) * slot_words;
-  };
-  // lane k < kStage: request the record of slot k of batch jj (cp.async, 16 bytes)
-  auto fetch_rec = [&](uint32_t jj, uint32_t e0, uint32_t e1) {
-    if (lane < kStage) {
-      const uint32_t i = e0 + w + uint32_t(lane) * kEngineWarps;
-      if (jj < nb && i < e1) cp_async16(&srec[jj % 4][w][lane], a.erec + i);
-      else srec[jj % 4][w][lane] = make_uint4(0xffffffffu, 0, 0, 0);
-    }
-  };
-  // stage batch jj's ready slots (lane k < kStage holds slot k's readiness + record)
-  auto stage_batch = [&](uint32_t jj, uint32_t e0, uint32_t ready, uint4 r) {
-#pragma unroll
-    for (int kk = 0; kk < kStage; ++kk) {
-      const uint32_t ok = __shfl_sync(kFull, ready, kk);
-      const uint32_t u = __shfl_sync(kFull, r.x, kk), cb = __shfl_sync(kFull, r.y, kk);
-      const uint32_t i = e0 + w + uint32_t(kk) * kEngineWarps;
-      if (ok) {
-        char* dst = reinterpret_cast<char*>(slotp(jj & 1, kk));
-        const uint32_t psl = __shfl_sync(kFull, r.w, kk);
-        const char* P = reinterpret_cast<const char*>(a.epart + size_t(psl) * d);
-        const char* Z = reinterpret_cast<const char*>(a.zold + size_t(u) * d);
-        const char* R = reinterpret_cast<const char*>(a.rl + size_t(i) * kRefStride);
-        for (uint32_t off = lane * 16; off < d * 8; off += 512) cp_async16(dst + off, P + off);
-        for (uint32_t off = lane * 16; off < d * 4; off += 512)
-          cp_async16(dst + d * 8 + off, Z + off);
-        if (lane * 16 < kRefStride * 4) cp_async16(dst + d * 12 + lane * 16, R + lane * 16);
-      }
-      if (lane == 0) staged[jj & 1][w][kk] = ok;
-    }
-  };
-  // prologue: records of batches 0..2, staging of batches 0 and 1
-  uint32_t c0 = cum(0), c1 = cum(1), c2 = cum(2), c3 = cum(3), c4 = cum(4);
-  fetch_rec(0, c0, c1);
-  fetch_rec(1, c1, c2);
-  fetch_rec(2, c2, c3);
-  cp_async_commit();
-  cp_async_wait_all();
-  __syncwarp();
-  for (uint32_t jj = 0; jj < 2; ++jj) {
-    uint32_t ready = 0;
-    uint4 r = make_uint4(0xffffffffu, 0, 0, 0);
-    if (lane < kStage) {
-      r = srec[jj % 4][w][lane];
-      if (r.x != 0xffffffffu) ready = ld_relaxed(a.vflag + r.x) == 2u;
-    }
-    stage_batch(jj, jj == 0 ? c0 : c1, ready, r);
-  }
-  cp_async_commit();
-  uint32_t waits = 0;
-  unsigned long long wait_ns = 0;
-  for (uint32_t j = 0; j < nb; ++j) {
-    if (a.etrace && threadIdx.x == 0) a.etrace[3ull * j] = globaltimer();
-    // every group but the newest (batch j+1's staging) has landed: batch j's staging
-    // and batch j+2's records
-    cp_async_wait_group<1>();
-    __syncwarp();
-    fetch_rec(j + 3, c3, c4);
-    cp_async_commit();
-    const uint32_t c5 = j + 5 <= nb ? cum(j + 5) : c4;
-    uint32_t ready = 0;
-    uint4 nrec = make_uint4(0xffffffffu, 0, 0, 0);
-    if (lane < kStage && j + 2 < nb) {  // readiness of batch j+2 (non-blocking load)
-      nrec = srec[(j + 2) % 4][w][lane];
-      if (nrec.x != 0xffffffffu) ready = ld_relaxed(a.vflag + nrec.x) == 2u;
-    }
-    int k = 0;
-    for (uint32_t i = c0 + w; i < c1; i += kEngineWarps, ++k) {
-      uint4 rec;
-      if (k < kStage) rec = srec[j % 4][w][k];
-      else rec = __ldg(a.erec + i);
-      const uint32_t u = rec.x, cb = rec.y, p = rec.z;
-      if (a.ltrace && lane == 0) a.ltrace[4ull * p + 3] = globaltimer();
-      float zu[K];
-      double acc[K];
-      uint32_t nrefs, myref = 0;
-      const bool st = k < kStage && staged[j & 1][w][k];
-      if (st) {
-        const uint32_t* sl = slotp(j & 1, k);
-        const double* sP = reinterpret_cast<const double*>(sl);
-        const float* sZ = reinterpret_cast<const float*>(reinterpret_cast<const char*>(sl) + d * 8);
-        const uint32_t* sR = reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(sl) +
-                                                                d * 12);
-#pragma unroll
-        for (int kk = 0; kk < K; ++kk) acc[kk] = sP[L::col(lane, kk)];
-        L::load_smem(sZ, lane, d, zu);
-        nrefs = sR[0];
-        if (lane < int(nrefs)) myref = sR[1 + lane];
-      } else {
-        const unsigned long long t0 = a.etrace ? globaltimer() : 0ull;
-        uint32_t f = ld_relaxed(a.vflag + u);
-        while (f != 2u) {  // the L items' pre-final partial
-          __nanosleep(20);
-          f = ld_relaxed(a.vflag + u);
-        }
-        if (a.etrace) {
-          ++waits;
-          wait_ns += globaltimer() - t0;
-        }
-        L::load_acc(a.epart + size_t(rec.w) * d, lane, d, acc);
-        L::load(a.zold + size_t(u) * d, lane, d, zu, false);
-        const uint32_t* R = a.rl + size_t(i) * kRefStride;
-        nrefs = __ldcg(R);
-        if (lane < int(nrefs)) myref = __ldcg(R + 1 + lane);
-      }
-      double lsum = (MON && lane == 0) ? __ldcg(a.eloss + cb) : 0.0;
-      Rows<KIND, K, VEC, MON, FAST>::template run<true, true>(a.fp, myref, int(nrefs), lane, d,
-                                                              a.zold, a.znew, zu, acc, lsum,
-                                                              ring);
-      const uint32_t es = i - c0;
-      float* rrow = es < a.maxe ? ring + (size_t(j % RS) * a.maxe + es) * d : nullptr;
-      finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum, rrow);
-      if (lane == 0) a.vflag[u] = 0;
-    }
-    if (a.etrace && lane == 0) atomicMax(a.etrace + 3ull * j + 1, globaltimer());
-    __syncwarp();
-    if (j + 2 < nb) stage_batch(j + 2, c2, ready, nrec);  // into buffer (j & 1), now free
-    cp_async_commit();
-    __syncthreads();  // batch j's ring rows are visible to batch j+1
-    if (a.etrace && threadIdx.x == 0) a.etrace[3ull * j + 2] = globaltimer();
-    c0 = c1;
-    c1 = c2;
-    c2 = c3;
-    c3 = c4;
-    c4 = c5;
-  }
-  cp_async_wait_all();
-  if (a.etrace && lane == 0 && waits) {
-    atomicAdd(a.etrace + 3ull * nb, (unsigned long long)waits);
-    atomicAdd(a.etrace + 3ull * nb + 1, wait_ns);
-  }
-}
-
-template <int KIND, int K, bool VEC, bool MON, bool FAST>
-void launch_engine(Ctx& c, const EpochArgs& a) {
-  if constexpr (!VEC) {
-    fail(F2V_EUSAGE, "chain engine requires the vector row layout");
-  } else {
-  auto kern = engine_kernel<KIND, K, VEC, MON, FAST>;
-  const size_t slot_words = (size_t(a.d) * 12 + kRefStride * 4 + 15) / 16 * 4;
-  const size_t smem = size_t(a.Re + 1) * a.maxe * a.d * sizeof(float) +
-                      2 * size_t(kEngineWarps) * kStage * slot_words * 4;
-  F2V_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  kern<<<1, kEngineWarps * 32, smem, c.stream2>>>(a);
-  F2V_LAUNCHED(c.stream2, "engine_kernel");
-  ++c.launches;
-  }
-}
-
 // Launch one epoch kernel instantiation as a persistent grid.
 template <int KIND, int K, bool VEC, bool MON, bool FAST, int MINB>
 void launch_one(Ctx& c, const EpochArgs& a) {
@@ -755,26 +512,12 @@ void launch_one(Ctx& c, const EpochArgs& a) {
   if (c.tune.ctas && int(c.tune.ctas) < per_sm) per_sm = int(c.tune.ctas);
   if (per_sm < 1) per_sm = 1;
   uint32_t blocks = uint32_t(per_sm) * uint32_t(c.num_sms);
-  if (a.Re) {
-    // the engine runs concurrently on stream2 (after the prep); leave it room
-    // on any SM (its 16 warps and ring fit beside one epoch CTA) so the two
-    // are co-resident whichever starts first
-    F2V_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    F2V_CUDA(cudaEventRecord(c.ev_prep, c.stream));
-    F2V_CUDA(cudaStreamWaitEvent(c.stream2, c.ev_prep, 0));
-    launch_engine<KIND, K, VEC, MON, FAST>(c, a);
-    blocks = blocks > 2 ? blocks - 2 : 1;
-  }
   const uint64_t ew = kWarps - a.lwarps;
   const uint32_t need = uint32_t(std::max<uint64_t>((a.n_eitems + ew - 1) / ew, 1));
-  blocks = std::max(1u, std::min(blocks, need + (a.Re ? 1u : 0u)));
+  blocks = std::max(1u, std::min(blocks, need));
   kern<<<blocks, kWarps * 32, 0, c.stream>>>(a);
   F2V_LAUNCHED(c.stream, "kern");
   ++c.launches;
-  if (a.Re) {
-    F2V_CUDA(cudaEventRecord(c.ev_engine, c.stream2));
-    F2V_CUDA(cudaStreamWaitEvent(c.stream, c.ev_engine, 0));
-  }
 }
 
 template <int KIND, int K, bool VEC, bool FAST>

@@ -45,14 +45,13 @@ struct DeviceBuf {
 // be overridden by the environment variable named beside it.
 struct EpochTuning {
   uint32_t chunk = 256;  // F2V_CHUNK: max arcs per E item (hub splitting)
-  uint32_t lgroup = 8;   // F2V_LGROUP: E chunks per L item
+  uint32_t lgroup = 16;  // F2V_LGROUP: E chunks per L item
   uint32_t window = 48;  // F2V_WINDOW: arcs to batches [j-window, j) go to L items
   uint32_t recent = 8;   // F2V_RECENT: window arcs this recent are taken last
   uint32_t lwarps = 1;   // F2V_LWARPS: L-role warps per 8-warp CTA
   uint32_t fast = 1;     // F2V_PRECISION=exact|fast: pair math precision (config)
   uint32_t ctas = 0;     // F2V_CTAS: resident epoch CTAs per SM (0 = as many as fit)
   uint32_t minb = 0;     // F2V_MINB: epoch register budget 2 or 3 CTAs/SM (0 = autotune)
-  uint32_t erecent = 0;  // F2V_ERECENT: chain engine takes arcs of age <= this (0 = off; opt-in)
 };
 void load_tuning(EpochTuning& t);
 
@@ -87,10 +86,6 @@ struct Ctx {
   DeviceBuf perm, state, negs_all, negwin, items, litems, nE, nL, EP, LP, wtot, needs, scan_tmp,
       epart, eloss, wcnt, wl, lpart, lloss, ploss, counters, pcnt, pslot;
   uint32_t last_litems = 0;
-  DeviceBuf nEng, ecum, epos, eslot, eidx, rcnt;  // chain engine lists
-  cudaStream_t stream2 = nullptr;                 // the chain engine runs here
-  cudaEvent_t ev_prep = nullptr, ev_engine = nullptr;
-  uint32_t eff_re = 0, eff_maxe = 0;              // engine window / ring rows this epoch
   // occupancy autotune (FAST d = 128): kernel ms of the 2- and 3-CTA builds on
   // this graph + config (negative = not yet timed) and the build in use
   double occ_ms[2] = {-1.0, -1.0};

@@ -22,10 +22,6 @@ namespace dev {
 constexpr unsigned kFull = 0xffffffffu;
 
 constexpr uint32_t kNewBit = 0x80000000u;
-// chain engine only: bit 30 = the row lives in the engine's shared-memory ring
-// (index in the low 30 bits), so vertex ids must stay below 2^30
-constexpr uint32_t kRingBit = 0x40000000u;
-constexpr uint32_t kIdMask = 0x3fffffffu;
 
 // Znew rows hold this NaN bit pattern until their final value is stored: a
 // reader polls the row itself instead of a separate flag (one L2 round trip,
@@ -93,36 +89,6 @@ struct Lay {
         const uint32_t c = col(lane, k);
         v[k] = (VEC || c < d) ? (coherent ? __ldcg(row + c) : __ldg(row + c)) : 0.0f;
       }
-    }
-  }
-  // a row in shared memory (generic loads)
-  __device__ static __forceinline__ void load_smem(const float* row, int lane, uint32_t d,
-                                                   float (&v)[K]) {
-    if constexpr (VEC && K % 4 == 0) {
-#pragma unroll
-      for (int q = 0; q < K / 4; ++q) {
-        const float4 t = reinterpret_cast<const float4*>(row + lane * K)[q];
-        v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const uint32_t c = col(lane, k);
-        v[k] = (VEC || c < d) ? row[c] : 0.0f;
-      }
-    }
-  }
-  __device__ static __forceinline__ void store_smem(float* row, int lane, uint32_t d,
-                                                    const float (&v)[K]) {
-    if constexpr (VEC && K % 4 == 0) {
-#pragma unroll
-      for (int q = 0; q < K / 4; ++q)
-        reinterpret_cast<float4*>(row + lane * K)[q] =
-            make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    } else {
-#pragma unroll
-      for (int k = 0; k < K; ++k)
-        if (valid(lane, k, d)) row[col(lane, k)] = v[k];
     }
   }
   // a Znew row: re-load until no lane sees the sentinel (warp-uniform loop).
@@ -286,12 +252,11 @@ __device__ __forceinline__ void accumulate(const Term& t, int lane, const double
 // EXACT: everything fp64 in the reference's operation order (bitwise parity
 // in practice).  KIND < 0 = force kind chosen at run time.
 // lsum is a per-lane loss partial: the caller warp-sums it.
-template <int KIND, int K, bool VEC, int U, bool MON, bool ATT, bool RING = false>
+template <int KIND, int K, bool VEC, int U, bool MON, bool ATT>
 __device__ __forceinline__ void rows_exact(const ForceParams& fp, uint32_t packed, int cnt,
                                            int lane, uint32_t d, const float* __restrict__ zold,
                                            const float* __restrict__ znew, const float (&zu)[K],
-                                           double (&acc)[K], double& lsum,
-                                           const float* ring = nullptr) {
+                                           double (&acc)[K], double& lsum) {
   using L = Lay<K, VEC>;
   const int kind = KIND >= 0 ? KIND : fp.kind;
   const bool sig = kind == F2V_SIGMOID;
@@ -307,10 +272,7 @@ __device__ __forceinline__ void rows_exact(const ForceParams& fp, uint32_t packe
       pks[i] = pk;
       if (k0 + i < cnt) {
         const bool coh = (pk & kNewBit) != 0;
-        if (RING && (pk & kRingBit))
-          L::load_smem(ring + size_t(pk & kIdMask) * d, lane, d, v[i]);
-        else
-          L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, v[i], coh);
+        L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, v[i], coh);
       } else {
 #pragma unroll
         for (int k = 0; k < K; ++k) v[i][k] = 0.0f;
@@ -318,7 +280,7 @@ __device__ __forceinline__ void rows_exact(const ForceParams& fp, uint32_t packe
     }
 #pragma unroll
     for (int i = 0; i < U; ++i)  // Znew rows not yet final: poll
-      if (k0 + i < cnt && (pks[i] & kNewBit) && !(RING && (pks[i] & kRingBit)))
+      if (k0 + i < cnt && (pks[i] & kNewBit))
         L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, v[i]);
     double w[U][K], red[U], nw[U];
 #pragma unroll
@@ -512,12 +474,11 @@ __device__ __forceinline__ void fast_block(const ForceParams& fp, int k0, int cn
 // The rows of one call are gathered NB = F2V_FAST_INFLIGHT at a time (all
 // loads issued before any block is reduced: 16 x 512 B in flight per warp),
 // then reduced 8 at a time in order.
-template <int KIND, int K, bool MON, bool ATT, bool RING = false>
+template <int KIND, int K, bool MON, bool ATT>
 __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed, int cnt,
                                           int lane, uint32_t d, const float* __restrict__ zold,
                                           const float* __restrict__ znew, const float (&zu)[K],
-                                          double (&acc)[K], double& lsum,
-                                          const float* ring = nullptr) {
+                                          double (&acc)[K], double& lsum) {
   using L = Lay<K, true>;
   constexpr int NB = F2V_FAST_INFLIGHT;
   d = 32 * K;  // VEC layout: a compile-time row stride
@@ -530,11 +491,7 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
       pks[i] = pk;
       if (k0 + i < cnt) {
         const bool coh = (pk & kNewBit) != 0;
-        if (RING && (pk & kRingBit))
-          L::load_smem(ring + size_t(pk & kIdMask) * d, lane, d, w[i / 8][i % 8]);
-        else
-          L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, w[i / 8][i % 8],
-                  coh);
+        L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, w[i / 8][i % 8], coh);
       } else {
 #pragma unroll
         for (int k = 0; k < K; ++k) w[i / 8][i % 8][k] = 0.0f;
@@ -545,7 +502,7 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
       if (k0 + 8 * h >= cnt) break;
 #pragma unroll
       for (int i = 8 * h; i < 8 * h + 8; ++i)  // Znew rows not yet final: poll
-        if (k0 + i < cnt && (pks[i] & kNewBit) && !(RING && (pks[i] & kRingBit)))
+        if (k0 + i < cnt && (pks[i] & kNewBit))
           L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, w[h][i % 8]);
       fast_block<KIND, K, MON, ATT>(fp, k0 + 8 * h, cnt, lane, zu, w[h], acc, lsum);
     }
@@ -625,20 +582,18 @@ __device__ __forceinline__ void rows_lowd(const ForceParams& fp, uint32_t packed
 // The row-accumulation policy the epoch kernel is instantiated with.
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
 struct Rows {
-  template <bool ATT, bool RING = false>
+  template <bool ATT>
   __device__ static __noinline__ void run(const ForceParams& fp, uint32_t packed, int cnt,
                                              int lane, uint32_t d, const float* zold,
                                              const float* znew, const float (&zu)[K],
-                                             double (&acc)[K], double& lsum,
-                                             const float* ring = nullptr) {
+                                             double (&acc)[K], double& lsum) {
     if constexpr (FAST && K == 1 && !VEC)
       rows_lowd<KIND, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else if constexpr (FAST)
-      rows_fast<KIND, K, MON, ATT, RING>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum,
-                                         ring);
+      rows_fast<KIND, K, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else
-      rows_exact<KIND, K, VEC, 4, MON, ATT, RING>(fp, packed, cnt, lane, d, zold, znew, zu, acc,
-                                                  lsum, ring);
+      rows_exact<KIND, K, VEC, 4, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc,
+                                            lsum);
   }
 };
 

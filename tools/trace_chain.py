@@ -19,8 +19,6 @@ nbt = (n + b - 1) // b
 tr = np.zeros(5 * n + 3 * nbt + 2, np.uint64); nl = C.c_uint32()
 lib.f2v_debug_trace(dev._h, tr, C.byref(nl))
 fin = tr[:n].astype(np.float64); lt = tr[n:5*n].reshape(n, 4).astype(np.float64)
-et = tr[5*n:5*n+3*nbt].reshape(nbt, 3).astype(np.float64)
-print('engine unstaged waits', int(tr[-2]), 'wait ms', tr[-1] / 1e6)
 t0 = fin.min(); fin = (fin - t0) / 1e3
 has = lt[:, 0] > 0
 lt[has] = (lt[has] - t0) / 1e3
@@ -54,31 +52,3 @@ print("recent done - prev_done:", pc(lt[c2, 3] - pd))
 print("final - prev_done:", pc(fin[c2] - pd))
 print("final - recent done:", pc(fin[c2] - lt[c2, 3]))
 
-if et[:, 0].max() > 0:
-    et = (et - t0) / 1e3
-    comp = et[:, 1] - et[:, 0]; tail = et[:, 2] - et[:, 1]; step = np.diff(et[:, 0])
-    print("ENGINE step us: mean %.2f median %.2f p90 %.2f | compute median %.2f p90 %.2f | prefetch+barrier median %.2f" % (step.mean(), np.median(step), np.percentile(step, 90), np.median(comp), np.percentile(comp, 90), np.median(tail)))
-    print("engine total ms %.2f; first step at %.1f us" % ((et[-1, 2] - et[0, 0]) / 1e3, et[0, 0]))
-eng = (lt[:, 2] > 0) & (lt[:, 3] > 0)
-if eng.any():
-    e = np.where(eng)[0]
-    pb = e // b
-    estart = et[pb, 0]
-    print("engine vertices traced", len(e))
-    print("L claim - engine step start:", pc(lt[e, 0] - estart))
-    print("L vflag(E) seen - engine step start:", pc(lt[e, 1] - estart))
-    print("P ready - engine step start:", pc(lt[e, 2] - estart))
-    print("engine picks vertex - P ready:", pc(lt[e, 3] - lt[e, 2]))
-# host recount of engine candidates for this epoch's perm (Re = F2V_ERECENT)
-Re = int(os.environ.get("F2V_ERECENT", "8"))
-pos = np.empty(n, np.int64); pos[perm] = np.arange(n)
-bat = pos // b
-src = np.repeat(np.arange(n), np.diff(g.row_offsets).astype(np.int64))
-age = bat[src] - bat[g.col_indices]
-rec = (age >= 1) & (age <= Re)
-cand = np.zeros(n, bool); cand[src[rec]] = True
-cand &= deg <= 2048
-print("engine candidates: %d (%.1f per batch); recent arcs %d (%.1f per batch)" % (cand.sum(), cand.sum() / nb, rec.sum(), rec.sum() / nb))
-# those whose recent arcs hit another candidate (true chain vertices)
-hit = np.zeros(n, bool); hit[src[rec & cand[g.col_indices]]] = True; hit &= cand
-print("candidates with a recent arc to a candidate: %d (%.1f per batch)" % (hit.sum(), hit.sum() / nb))
