@@ -216,6 +216,16 @@ __global__ void zero_kernel(double* __restrict__ v, uint64_t m) {
   if (i < m) v[i] = 0.0;
 }
 
+// debug switches are honoured by debug builds only (-DF2V_DEBUG_BUILD)
+bool debug_env(const char* name) {
+#ifdef F2V_DEBUG_BUILD
+  return std::getenv(name) != nullptr;
+#else
+  (void)name;
+  return false;
+#endif
+}
+
 uint32_t env_u32(const char* name, uint32_t dflt) {
   if (const char* e = std::getenv(name)) {
     const long v = std::atol(e);
@@ -419,7 +429,7 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
       c.perm.as<uint32_t>(), geo, c.state.as<uint32_t>(), c.wtot.as<uint32_t>(),
       c.negwin.as<uint32_t>(), c.lbase.as<uint32_t>(), c.cbase.as<uint32_t>(),
       c.needs.as<uint32_t>(), c.nL.as<uint32_t>(), c.pcnt.as<uint32_t>(),
-      std::getenv("F2V_DEBUG_NODEP") ? 1 : 0);
+      debug_env("F2V_DEBUG_NODEP") ? 1 : 0);
   F2V_LAUNCHED(c.stream, "needs_kernel");
   size_t tmp = 0;
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.nE.as<uint32_t>(), c.EP.as<uint32_t>(),
@@ -537,13 +547,13 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
       if (int32_t(g) != c.rank) a.peer_znew[a.npeers++] = c.peer_z[g][nxt];
   a.eta = eta;
   a.fp = fp;
-  a.nodep = std::getenv("F2V_DEBUG_NODEP") ? 1 : 0;
+  a.nodep = debug_env("F2V_DEBUG_NODEP") ? 1 : 0;
   a.nnz = c.nnz;
   a.chunks = c.chunks;
   a.lslots = c.lslots;
   a.trace = nullptr;
   a.ltrace = nullptr;
-  if (std::getenv("F2V_TRACE")) {
+  if (debug_env("F2V_TRACE")) {
     const uint32_t nbt = c.steps;
     c.trace.ensure(sizeof(unsigned long long) * (5ull * std::max<uint32_t>(c.n, 1) + 3ull * nbt + 2));
     a.trace = c.trace.as<unsigned long long>();

@@ -108,6 +108,22 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   } while (0)
 #endif
 
+// Debug instrumentation (F2V_DEBUG_NODEP, F2V_TRACE) is compiled in only for
+// debug builds (F2V_NVCC_EXTRA=-DF2V_DEBUG_BUILD): the epoch kernel is
+// instruction-fetch sensitive, so release builds carry none of it.
+#ifdef F2V_DEBUG_BUILD
+#define F2V_NODEP(a) ((a).nodep)
+#define F2V_STAMP(ptr, idx) \
+  do {                      \
+    if (ptr) (ptr)[idx] = globaltimer(); \
+  } while (0)
+#else
+#define F2V_NODEP(a) false
+#define F2V_STAMP(ptr, idx) \
+  do {                      \
+  } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
 // shard g owns rows [floor(n g / G), floor(n (g+1) / G)) (orc_shard_range)
@@ -165,7 +181,7 @@ __device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, uin
     if (lane < cnt) {
       const uint32_t w = a.negs[size_t(q) * a.s + k0 + lane];
       const uint32_t st = ld_relaxed(a.state + w);
-      if ((st >> 1) < j && !a.nodep) {
+      if ((st >> 1) < j && !F2V_NODEP(a)) {
         pk = w | kNewBit;  // Znew row: the row loads poll its sentinel
       } else {
         pk = w;
@@ -209,7 +225,7 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_
   }
   if (lane == 0) {
     if (any_bad) atomicMin(a.bad, (unsigned long long)p);
-    if (a.trace) a.trace[p] = globaltimer();
+    F2V_STAMP(a.trace, p);
   }
 }
 
@@ -244,7 +260,7 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
       DCHECK(v < a.n, "E v=%u", v);
       const uint32_t st = ld_relaxed(a.state + v);
       const uint32_t bv = st >> 1;
-      if (bv >= j || a.nodep) {
+      if (bv >= j || F2V_NODEP(a)) {
         use = true;
         pk = v;
       } else if (bv + a.W < j) {  // past: final long ago (the row load rarely polls)
@@ -408,8 +424,10 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   const uint32_t cb = a.cbase[u];
   const uint32_t nch = a.cbase[u + 1] - cb;
   const uint32_t nchL = a.lbase[u + 1] - a.lbase[u];
+#ifdef F2V_DEBUG_BUILD
   unsigned long long* lt = (a.ltrace && cl == 0) ? a.ltrace + 4ull * p : nullptr;
-  if (lt && lane == 0) lt[0] = globaltimer();
+#endif
+  if (lane == 0) F2V_STAMP(lt, 0);
   float zu[K];
   L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
   double acc[K];
@@ -422,7 +440,7 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     __nanosleep(64);
     f = ld_relaxed(a.vflag + u);
   }
-  if (lt && lane == 0) lt[1] = globaltimer();
+  if (lane == 0) F2V_STAMP(lt, 1);
   const uint32_t c0 = cl * a.G, c1 = umin32(nch, c0 + a.G);
   const uint32_t ps = __ldg(a.pslot + p);  // the E total of u lives in partial slot ps
   if (nchL == 1) {
@@ -432,9 +450,9 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     // E total + old window arcs + negatives + recent arcs
     window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
     do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
-    if (lt && lane == 0) lt[2] = globaltimer();
+    if (lane == 0) F2V_STAMP(lt, 2);
     recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
-    if (lt && lane == 0) lt[3] = globaltimer();
+    if (lane == 0) F2V_STAMP(lt, 3);
     finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
     if (lane == 0) a.vflag[u] = 0;
     return;

@@ -1,4 +1,5 @@
-"""DEBUG: per-batch completion profile of one C2 epoch (F2V_TRACE=1)."""
+"""DEBUG: per-batch completion profile of one C2 epoch (F2V_TRACE=1).
+Needs a debug build: F2V_NVCC_EXTRA=-DF2V_DEBUG_BUILD python paper_2009_10035_b200/build.py --force"""
 import ctypes as C, os, sys, json
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
