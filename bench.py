@@ -272,7 +272,9 @@ def bench_b200(args):
                           epochs=args.warmup + args.steps,
                           model=f2v.ForceModel(f2v.ForceKind.parse(kind)), seed=1,
                           monitor_loss=False, sampler="philox")
-    if world > 1:
+    # F2V_BENCH_SHARDED=1 runs the sharded code path at world 1 as well
+    sharded = world > 1 or bool(os.environ.get("F2V_BENCH_SHARDED"))
+    if sharded:
         # vertex-partitioned shards: each GPU runs its
         # rows and stores every updated row into all replicas over NVLink
         from paper_2009_10035_b200.dist import ShardedDevice
@@ -340,11 +342,11 @@ def bench_b200(args):
     cfg_e2e = f2v.TrainConfig(dim=d, batch=b, negatives=s, lr=lr, epochs=epochs,
                               model=cfg.model, seed=1, monitor_loss=False, sampler="philox")
 
-    if world > 1:
+    if sharded:
         cfg_e2e = dataclasses.replace(cfg_e2e, shards=world)
 
     def e2e_once():
-        if world > 1:  # the public sharded API, from host buffers
+        if sharded:  # the public sharded API, from host buffers
             s2 = ShardedDevice(rank, world, local)
             s2.setup(g_pinned, h_z0)
             s2.train_epochs(cfg_e2e)
