@@ -1,13 +1,7 @@
 // f2v_epoch.cuh -- the persistent dataflow epoch kernel (see f2v_epoch.cu for
 // the schedule).  Instantiated per (force kind, row layout, loss monitoring,
-// precision) in f2v_epoch_fast.cu / f2v_epoch_exact.cu.
+// precision, register budget) in the f2v_epoch_i_*.cu translation units.
 #pragma once
-#include <algorithm>
-
-#include "f2v_internal.h"
-#include "f2v_pair.cuh"
-#include "f2v_rng.h"
-
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>

@@ -1,5 +1,6 @@
-// f2v_internal.h -- device context shared by the C-ABI (f2v_capi.cpp), the
-// host driver (f2v_host.cpp) and the kernels (f2v_kernels.cu).
+// f2v_internal.h -- the device context shared by the C-ABI and host driver
+// (f2v_capi.cpp), the host data formats (f2v_graph.cpp) and the kernels
+// (f2v_step.cu, f2v_epoch*.cu, f2v_perm.cu, f2v_walk.cu, f2v_shard.cu).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -127,7 +128,7 @@ struct Ctx {
   float* zcur() const { return z[cur].as<float>(); }
 };
 
-// kernels (f2v_kernels.cu)
+// kernels
 void k_grad_minibatch(Ctx& c, uint32_t b, uint32_t s, const ForceParams& fp, bool want_loss);
 void k_apply_update(Ctx& c, uint32_t b, float eta, bool unique_ids);
 double k_batch_loss_sum(Ctx& c, uint32_t b);
