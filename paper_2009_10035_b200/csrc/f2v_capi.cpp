@@ -270,7 +270,7 @@ void f2v_destroy(f2v_ctx* h) {
   cudaSetDevice(h->c.device);
   Ctx& c = h->c;
   for (DeviceBuf* b :
-       {&c.rowptr, &c.col, &c.cbase, &c.lbase, &c.lpo, &c.src, &c.ecnt, &c.lcnt, &c.vflag,
+       {&c.rowptr, &c.col, &c.cbase, &c.lbase, &c.lpo, &c.ecnt, &c.lcnt, &c.vflag,
         &c.z[0], &c.z[1], &c.grads, &c.ids, &c.negs, &c.vloss, &c.bad, &c.scratch, &c.perm,
         &c.state, &c.negs_all, &c.negwin, &c.items, &c.litems, &c.nE, &c.nL, &c.EP, &c.LP,
         &c.wtot, &c.needs, &c.scan_tmp, &c.epart, &c.eloss, &c.wcnt, &c.wl, &c.lpart, &c.lloss,

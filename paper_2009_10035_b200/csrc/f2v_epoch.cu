@@ -78,26 +78,27 @@ __global__ void scatter_kernel(const uint32_t* __restrict__ lperm, const uint32_
   wtot[u] = 0;
 }
 
-// One thread per arc: mark the vertices that have a window arc (batch(v) in
-// [batch(u) - W, batch(u))).  src[] is the static arc -> source map.
-__global__ void window_scan_kernel(const uint32_t* __restrict__ src,
+// Mark the vertices that have a window arc (batch(v) in [batch(u) - W,
+// batch(u))): one warp per E item (its vertex and arc range are resolved), so
+// the step of u is read once per item and one atomic per item sets the flag.
+__global__ void window_scan_kernel(const ep::EItem* __restrict__ items,
+                                   const uint32_t* __restrict__ n_items,
                                    const uint32_t* __restrict__ col,
                                    const uint32_t* __restrict__ state, uint32_t* __restrict__ wtot,
-                                   uint64_t nnz, uint32_t W) {
-  const uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (e >= nnz) return;
-  const uint32_t u = __ldg(src + e), v = __ldg(col + e);
-  const uint32_t j = __ldg(state + u) >> 1, bv = __ldg(state + v) >> 1;
-  if (bv < j && bv + W >= j) atomicOr(wtot + u, 1u);
-}
-
-// src[e] = the row of arc e (static per graph)
-__global__ void src_kernel(const uint64_t* __restrict__ rowptr, uint32_t* __restrict__ src,
-                           uint32_t n) {
-  const uint32_t u = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+                                   uint32_t W) {
   const int lane = threadIdx.x & 31;
-  if (u >= n) return;
-  for (uint64_t e = rowptr[u] + lane; e < rowptr[u + 1]; e += 32) src[e] = u;
+  const uint32_t total = *n_items;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < total; it += nw) {
+    const ep::EItem item = items[it];
+    const uint32_t j = __ldg(state + item.u) >> 1;
+    bool win = false;
+    for (uint32_t t = lane; t < item.cnt; t += 32) {
+      const uint32_t bv = __ldg(state + __ldg(col + item.e0 + t)) >> 1;
+      win |= bv < j && bv + W >= j;
+    }
+    if (__any_sync(0xffffffffu, win) && lane == 0) atomicOr(wtot + item.u, 1u);
+  }
 }
 
 __global__ void needs_kernel(const uint32_t* __restrict__ perm, ShardGeo geo,
@@ -277,7 +278,6 @@ void k_prepare_graph(Ctx& c) {
   c.cbase.ensure(sizeof(uint32_t) * (size_t(c.n) + 1));
   c.lbase.ensure(sizeof(uint32_t) * (size_t(c.n) + 1));
   c.lpo.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
-  c.src.ensure(sizeof(uint32_t) * std::max<uint64_t>(c.nnz, 1));
   c.ecnt.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
   c.lcnt.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
   c.vflag.ensure(sizeof(uint32_t) * std::max<uint32_t>(c.n, 1));
@@ -285,11 +285,6 @@ void k_prepare_graph(Ctx& c) {
                            cudaMemcpyHostToDevice, c.stream));
   F2V_CUDA(cudaMemcpyAsync(c.lbase.p, lbase.data(), sizeof(uint32_t) * (c.n + 1),
                            cudaMemcpyHostToDevice, c.stream));
-  if (c.n) {
-    src_kernel<<<uint32_t((uint64_t(c.n) * 32 + 255) / 256), 256, 0, c.stream>>>(
-        c.rowptr.as<uint64_t>(), c.src.as<uint32_t>(), c.n);
-    F2V_LAUNCHED(c.stream, "src_kernel");
-  }
   if (c.n) {
     F2V_CUDA(cudaMemcpyAsync(c.lpo.p, lpo.data(), sizeof(uint32_t) * c.n,
                              cudaMemcpyHostToDevice, c.stream));
@@ -420,23 +415,28 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
       seed, epoch, sampler, W, c.walk_k, c.walk_k ? c.wpos.as<uint32_t>() : nullptr,
       c.poff.as<uint32_t>());
   F2V_LAUNCHED(c.stream, "negs_kernel");
-  if (c.nnz)
-    window_scan_kernel<<<uint32_t((c.nnz + 255) / 256), 256, 0, c.stream>>>(
-        c.src.as<uint32_t>(), c.col.as<uint32_t>(), c.state.as<uint32_t>(),
-        c.wtot.as<uint32_t>(), c.nnz, W);
-  F2V_LAUNCHED(c.stream, "window_scan_kernel");
-  needs_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
-      c.perm.as<uint32_t>(), geo, c.state.as<uint32_t>(), c.wtot.as<uint32_t>(),
-      c.negwin.as<uint32_t>(), c.lbase.as<uint32_t>(), c.cbase.as<uint32_t>(),
-      c.needs.as<uint32_t>(), c.nL.as<uint32_t>(), c.pcnt.as<uint32_t>(),
-      debug_env("F2V_DEBUG_NODEP") ? 1 : 0);
-  F2V_LAUNCHED(c.stream, "needs_kernel");
   size_t tmp = 0;
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, c.nE.as<uint32_t>(), c.EP.as<uint32_t>(),
                                          n + 1, c.stream));
   c.scan_tmp.ensure(tmp);
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.nE.as<uint32_t>(),
                                          c.EP.as<uint32_t>(), n + 1, c.stream));
+  emit_e_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(
+      c.EP.as<uint32_t>(), c.perm.as<uint32_t>(), c.cbase.as<uint32_t>(),
+      c.rowptr.as<uint64_t>(), c.items.as<ep::EItem>(), n, c.tune.chunk);
+  F2V_LAUNCHED(c.stream, "emit_e_kernel");
+  if (c.nnz) {
+    window_scan_kernel<<<uint32_t(c.num_sms) * 16, 256, 0, c.stream>>>(
+        c.items.as<ep::EItem>(), c.EP.as<uint32_t>() + n, c.col.as<uint32_t>(),
+        c.state.as<uint32_t>(), c.wtot.as<uint32_t>(), W);
+    F2V_LAUNCHED(c.stream, "window_scan_kernel");
+  }
+  needs_kernel<<<(n + 1 + 255) / 256, 256, 0, c.stream>>>(
+      c.perm.as<uint32_t>(), geo, c.state.as<uint32_t>(), c.wtot.as<uint32_t>(),
+      c.negwin.as<uint32_t>(), c.lbase.as<uint32_t>(), c.cbase.as<uint32_t>(),
+      c.needs.as<uint32_t>(), c.nL.as<uint32_t>(), c.pcnt.as<uint32_t>(),
+      debug_env("F2V_DEBUG_NODEP") ? 1 : 0);
+  F2V_LAUNCHED(c.stream, "needs_kernel");
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.nL.as<uint32_t>(),
                                          c.LP.as<uint32_t>(), n + 1, c.stream));
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.pcnt.as<uint32_t>(),
@@ -460,10 +460,6 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
       c.epart.ensure(sizeof(double) * std::max<uint64_t>(uint64_t(slots) * c.d, 1));
     }
   }
-  emit_e_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(
-      c.EP.as<uint32_t>(), c.perm.as<uint32_t>(), c.cbase.as<uint32_t>(),
-      c.rowptr.as<uint64_t>(), c.items.as<ep::EItem>(), n, c.tune.chunk);
-  F2V_LAUNCHED(c.stream, "emit_e_kernel");
   emit_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(c.LP.as<uint32_t>(), c.nL.as<uint32_t>(),
                                                      c.litems.as<uint2>(), n);
   F2V_LAUNCHED(c.stream, "emit_kernel");

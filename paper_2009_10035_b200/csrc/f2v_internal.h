@@ -70,7 +70,7 @@ struct Ctx {
   DeviceBuf rowptr, col;
   std::vector<uint64_t> h_rowptr;  // host copy: degrees for counters/partials
   // chunk / L-group layout, static per (graph, chunk, lgroup)
-  DeviceBuf cbase, lbase, lpo, src, ecnt, lcnt, vflag;
+  DeviceBuf cbase, lbase, lpo, ecnt, lcnt, vflag;
   uint64_t chunks = 0, lgroups = 0, lslots = 0;
   uint32_t prepared_chunk = 0, prepared_lgroup = 0;
 
