@@ -505,3 +505,66 @@ def test_exact_partial_sizing_identical(f2v, orc):
         finally:
             os.environ.pop("F2V_EPART_EXACT", None)
     assert outs[0][0] == outs[1][0] and np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.slow
+def test_full_size_config2_epoch_parity(f2v, orc, dev):
+    """BASELINE config 2 at full size (R-MAT 20: 1,048,576 vertices, 31.4M
+    arcs, d = 128, t-dist, b = 384, Philox negatives, U(-1,1) Z): one device
+    epoch (FAST, the bench path) against the oracle's epoch from the same Z --
+    per-row |dz|/|z| <= 1e-5 and the epoch loss within 1e-3 (north_star)."""
+    g = f2v.rmat_graph(20, 16, seed=1)
+    n = g.num_vertices()
+    dev.upload_graph(g)
+    dev.uniform_embedding(n, 128, 1)
+    z0 = dev.get_embedding()
+    cfg = f2v.TrainConfig(dim=128, batch=384, negatives=5, lr=0.02, epochs=5,
+                          model=kind_model(f2v, "tdist"), seed=1, monitor_loss=True,
+                          sampler="philox")
+    ctr = f2v.TrainCounters()
+    losses = dev.train_epochs(cfg, 0, 1, counters=ctr)
+    z = dev.get_embedding()
+    rc, zr, lr_, cr, _ = orc.orc_train(g.row_offsets, g.col_indices, z0, 384, 5, 0.02, 1, "tdist",
+                                       1, sampler="philox", threads=os.cpu_count() or 8)
+    assert rc == 0
+    z_parity(z, zr)
+    assert abs(losses[0] - lr_[0]) <= 1e-3 * abs(lr_[0])
+    assert [ctr.attractive_evals, ctr.repulsive_evals] == [int(cr[0]), int(cr[1])]
+
+
+@pytest.mark.slow
+def test_full_size_config3_epoch_parity(f2v, orc, dev):
+    """BASELINE config 3 at full size (Chung-Lu n = 3M, ~230M arcs, sigmoid,
+    d = 128, b = 384, U(-1,1) Z): one epoch on both sides from the same Z.
+
+    This config is chaotic within one epoch (rows grow ~500x; the epoch loss
+    reaches ~1e13), so any rounding difference is amplified down the batch
+    chain.  The north_star tolerances are per step and per epoch loss:
+      * FAST (the bench path): rows updated in the first 100 batches -- whose
+        inputs are still (nearly) the shared initial Z -- agree to 1e-5, and
+        the epoch loss to 1e-3;
+      * EXACT: the whole epoch's Z is bit-identical to the oracle's (checked
+        to 1e-5 row-relative) and the loss agrees to 1e-9."""
+    g = f2v.chung_lu_graph(3_000_000, 2.2, 2.0, 30000.0, 78.0, 1)
+    n = g.num_vertices()
+    dev.upload_graph(g)
+    dev.uniform_embedding(n, 128, 1)
+    z0 = dev.get_embedding()
+    rc, zr, lr_, _, _ = orc.orc_train(g.row_offsets, g.col_indices, z0, 384, 5, 0.02, 1,
+                                      "sigmoid", 1, sampler="philox",
+                                      threads=os.cpu_count() or 8)
+    assert rc == 0
+    first = dev.partition_epoch(n, 384, 1, 0)[:100 * 384]  # batches 0..99 (train()'s perm)
+    for precision in ("fast", "exact"):
+        dev.set_embedding(z0)
+        cfg = f2v.TrainConfig(dim=128, batch=384, negatives=5, lr=0.02, epochs=1,
+                              model=kind_model(f2v, "sigmoid"), seed=1, monitor_loss=True,
+                              sampler="philox", precision=precision)
+        losses = dev.train_epochs(cfg)
+        z = dev.get_embedding()
+        if precision == "fast":
+            z_parity(z, zr, rows=first)
+            assert abs(losses[0] - lr_[0]) <= 1e-3 * abs(lr_[0])
+        else:
+            z_parity(z, zr)
+            assert abs(losses[0] - lr_[0]) <= 1e-9 * abs(lr_[0])
