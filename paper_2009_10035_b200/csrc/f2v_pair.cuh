@@ -509,6 +509,120 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
   }
 }
 
+// ------------------------------------------------------- EXACT, transposed
+// EXACT (fp64 in the reference's operation order) for the VEC layouts, 8
+// pairs at a time: per-lane fp64 partial dots as in rows_exact, then a
+// transposed fp64 reduction (4+2+1 exchange rounds leave each 4-lane group
+// one pair's total), so the fp64 force term (exp / div / sqrt) of 8 pairs is
+// evaluated once, in parallel, instead of redundantly on all 32 lanes; its
+// coefficients are broadcast and every lane accumulates its columns pair by
+// pair in the reference's order (accumulate<K>).  Only the cross-lane order
+// of the dot reduction differs from rows_exact (both are fp64 trees).
+__device__ __forceinline__ double reduce8d(double (&p)[8], int lane) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool hi = lane & 16;
+    const double send = hi ? p[i] : p[i + 4];
+    const double keep = hi ? p[i + 4] : p[i];
+    p[i] = __dadd_rn(keep, __shfl_xor_sync(kFull, send, 16));
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool hi = lane & 8;
+    const double send = hi ? p[i] : p[i + 2];
+    const double keep = hi ? p[i + 2] : p[i];
+    p[i] = __dadd_rn(keep, __shfl_xor_sync(kFull, send, 8));
+  }
+  {
+    const bool hi = lane & 4;
+    const double send = hi ? p[0] : p[1];
+    const double keep = hi ? p[1] : p[0];
+    p[0] = __dadd_rn(keep, __shfl_xor_sync(kFull, send, 4));
+  }
+  p[0] = __dadd_rn(p[0], __shfl_xor_sync(kFull, p[0], 2));
+  p[0] = __dadd_rn(p[0], __shfl_xor_sync(kFull, p[0], 1));
+  return p[0];
+}
+
+template <int KIND, int K, bool MON, bool ATT>
+__device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t packed, int cnt,
+                                            int lane, uint32_t d, const float* __restrict__ zold,
+                                            const float* __restrict__ znew, const float (&zu)[K],
+                                            double (&acc)[K], double& lsum) {
+  using L = Lay<K, true>;
+  const int kind = KIND >= 0 ? KIND : fp.kind;
+  const bool sig = kind == F2V_SIGMOID;
+  const int pi = pair_of_lane(lane);
+  d = 32 * K;  // VEC layout: a compile-time row stride
+  double uu[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) uu[k] = zu[k];
+  for (int k0 = 0; k0 < cnt; k0 += 8) {
+    float v[8][K];
+    uint32_t pks[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
+      pks[i] = pk;
+      if (k0 + i < cnt) {
+        const bool coh = (pk & kNewBit) != 0;
+        L::load((coh ? znew : zold) + size_t(pk & ~kNewBit) * d, lane, d, v[i], coh);
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) v[i][k] = 0.0f;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)  // Znew rows not yet final: poll
+      if (k0 + i < cnt && (pks[i] & kNewBit))
+        L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, v[i]);
+    double part[8], nrm[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      double s = 0.0, q = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const double o = double(v[i][k]);
+        if (sig) {
+          s = __dadd_rn(s, __dmul_rn(uu[k], o));
+          if (!ATT) q = __dadd_rn(q, __dmul_rn(o, o));
+        } else {
+          const double w = __dsub_rn(uu[k], o);
+          s = __dadd_rn(s, __dmul_rn(w, w));
+        }
+      }
+      part[i] = s;
+      nrm[i] = q;
+    }
+    const double red = reduce8d(part, lane);
+    const double nr = (sig && !ATT) ? reduce8d(nrm, lane) : 0.0;
+    const Term t = pair_term<MON>(kind, fp, ATT, red, nr);  // pair pi, once per 4-lane group
+    if (MON && (lane & 3) == 0 && k0 + pi < cnt) lsum = __dadd_rn(lsum, t.loss);
+    const int tflags = (t.fallback ? 1 : 0) | (t.clamped ? 2 : 0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int src = lane_of_pair(i);
+      Term ti;
+      ti.dist = !sig;
+      const int f = __shfl_sync(kFull, tflags, src);
+      ti.fallback = f & 1;
+      ti.clamped = (f & 2) != 0;
+      ti.coef = __shfl_sync(kFull, t.coef, src);
+      ti.inv = sig ? 1.0 : __shfl_sync(kFull, t.inv, src);
+      ti.scale = ti.clamped ? __shfl_sync(kFull, t.scale, src) : 1.0;
+      if (k0 + i < cnt) {
+        double w[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double o = double(v[i][k]);
+          w[k] = sig ? o : __dsub_rn(uu[k], o);
+        }
+        accumulate<K>(ti, lane, w, acc);
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------- FAST low-d
 // d <= kLowD (the 2-D layout config): rows are too narrow to fill a warp, so
 // each lane owns one PAIR of the call -- its row (d floats) is one 8/16-byte
@@ -591,6 +705,8 @@ struct Rows {
       rows_lowd<KIND, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else if constexpr (FAST)
       rows_fast<KIND, K, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
+    else if constexpr (VEC)
+      rows_exact8<KIND, K, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else
       rows_exact<KIND, K, VEC, 4, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc,
                                             lsum);
