@@ -28,11 +28,15 @@ constexpr uint32_t kNewBit = 0x80000000u;
 // no fence on the writer).  Finalised values are never this NaN.
 constexpr uint32_t kSentinel = 0xffc0ffeeu;
 
-template <int K>
+// STEP = 2 for rows written and read as 16-byte vectors (VEC, K % 4 == 0):
+// aligned 8-byte halves are accessed atomically (the assumption NCCL's LL
+// protocol also makes), so one float per half decides it.  Scalar layouts
+// check every float.
+template <int K, int STEP = 1>
 __device__ __forceinline__ bool has_sentinel(const float (&v)[K]) {
   bool b = false;
 #pragma unroll
-  for (int k = 0; k < K; ++k) b |= __float_as_uint(v[k]) == kSentinel;
+  for (int k = 0; k < K; k += STEP) b |= __float_as_uint(v[k]) == kSentinel;
   return b;
 }
 
@@ -97,7 +101,7 @@ struct Lay {
   __device__ static __forceinline__ void poll(const float* row, int lane, uint32_t d,
                                               float (&v)[K]) {
     uint32_t it = 0;
-    while (__any_sync(kFull, has_sentinel<K>(v))) {
+    while (__any_sync(kFull, has_sentinel<K, (VEC && K % 4 == 0) ? 2 : 1>(v))) {
       __nanosleep(20);
       load(row, lane, d, v, true);
       if (++it == (1u << 28)) __trap();
