@@ -243,6 +243,7 @@ void load_tuning(EpochTuning& t) {
   t.window = std::max(1u, env_u32("F2V_WINDOW", t.window));
   t.recent = env_u32("F2V_RECENT", t.recent);
   t.lwarps = std::min(uint32_t(ep::kWarps - 1), std::max(1u, env_u32("F2V_LWARPS", t.lwarps)));
+  t.lwarps_env = std::getenv("F2V_LWARPS") != nullptr;
   if (const char* e = std::getenv("F2V_PRECISION")) t.fast = std::strcmp(e, "exact") != 0;
   t.ctas = env_u32("F2V_CTAS", t.ctas);
   t.minb = env_u32("F2V_MINB", t.minb);
@@ -563,9 +564,10 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
     F2V_CUDA(cudaEventCreate(&c.ev_kernel[1]));
   }
   // Occupancy autotune (FAST d = 128): the second epoch of a (graph, config)
-  // (the first one runs cold: fresh buffers, TLB) runs with both register budgets on the same inputs -- the kernel only
-  // reads Zold, so the second run reproduces Znew exactly -- and the faster
-  // build is kept.  Results never depend on the choice (tested).
+  // (the first runs cold: fresh buffers, TLB) runs once per variant -- the
+  // register budget (2 or 3 CTAs/SM) and the L-role warps per CTA (1 or 2) --
+  // on the same inputs (the kernel only reads Zold, so every run reproduces
+  // Znew exactly), and the fastest is kept.  Results never depend on it (tested).
   const uint64_t key = (uint64_t(c.n) * 1000003ull + c.nnz) ^ (uint64_t(a.b) << 40) ^
                        (uint64_t(fp.kind) << 56) ^ (uint64_t(c.shards) << 60) ^
                        (uint64_t(monitor) << 63);
@@ -579,40 +581,61 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
     c.occ_key = key;
     c.occ_epochs = 0;
     c.occ_use = 2;
+    c.occ_lwarps = c.tune.lwarps;
   } else if (++c.occ_epochs == 1) {
     tune_now = true;
   }
+  if (tunable && !c.tune.lwarps_env) a.lwarps = c.occ_lwarps;
   auto launch_timed = [&]() {
     F2V_CUDA(cudaEventRecord(c.ev_kernel[0], c.stream));
     ep::launch_epoch(c, a, monitor, c.tune.fast != 0);
     F2V_CUDA(cudaEventRecord(c.ev_kernel[1], c.stream));
   };
   if (tune_now) {
+    struct Variant {
+      int minb;
+      uint32_t lwarps;
+    };
+    const uint32_t L0 = c.tune.lwarps;
+    const Variant vars[3] = {{2, L0}, {2, L0 + 1}, {3, L0}};
+    const int nv = c.tune.lwarps_env || L0 + 1 >= uint32_t(ep::kWarps) ? 2 : 3;
+    const Variant* vv = vars;
+    const Variant two[2] = {{2, L0}, {3, L0}};
+    if (nv == 2) vv = two;
     // load both builds first: with lazy module loading a first launch would
     // time the load as well
     c.dry_launch = true;
-    for (int v = 0; v < 2; ++v) {
-      c.occ_use = 2 + v;
+    for (int m = 2; m <= 3; ++m) {
+      c.occ_use = m;
       ep::launch_epoch(c, a, monitor, c.tune.fast != 0);
     }
     c.dry_launch = false;
-    float ms[2];
-    for (int v = 0; v < 2; ++v) {
+    float best = 0.f;
+    int bi = 0;
+    for (int v = 0; v < nv; ++v) {
       if (v) {  // reset the claim counters / first failure, Znew back to the sentinel
         F2V_CUDA(cudaMemsetAsync(ctr, 0, 8, c.stream));
         F2V_CUDA(cudaMemsetAsync(ctr + 2, 0xff, 8, c.stream));
         fill_sentinel();
       }
-      c.occ_use = 2 + v;
+      c.occ_use = vv[v].minb;
+      a.lwarps = vv[v].lwarps;
       launch_timed();
       F2V_CUDA(cudaEventSynchronize(c.ev_kernel[1]));
-      F2V_CUDA(cudaEventElapsedTime(&ms[v], c.ev_kernel[0], c.ev_kernel[1]));
-      c.occ_ms[v] = ms[v];
+      float ms = 0.f;
+      F2V_CUDA(cudaEventElapsedTime(&ms, c.ev_kernel[0], c.ev_kernel[1]));
+      if (v < 2) c.occ_ms[v] = ms;
+      if (std::getenv("F2V_DEBUG_OCC"))
+        std::fprintf(stderr, "f2v autotune: %d CTAs/SM, %u L warps: %.3f ms\n", vv[v].minb,
+                     vv[v].lwarps, ms);
+      if (v == 0 || ms < best) {
+        best = ms;
+        bi = v;
+      }
     }
-    c.occ_use = ms[1] < ms[0] ? 3 : 2;
-    if (std::getenv("F2V_DEBUG_OCC"))
-      std::fprintf(stderr, "f2v occupancy autotune: 2 CTAs/SM %.3f ms, 3 CTAs/SM %.3f ms\n", ms[0],
-                   ms[1]);
+    // Znew holds the last variant's (identical) epoch; keep the fastest
+    c.occ_use = vv[bi].minb;
+    c.occ_lwarps = vv[bi].lwarps;
   } else {
     launch_timed();
   }
