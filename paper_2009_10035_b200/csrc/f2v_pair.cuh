@@ -504,10 +504,18 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
 #pragma unroll
     for (int h = 0; h < NB / 8; ++h) {
       if (k0 + 8 * h >= cnt) break;
+      // Znew rows not yet final: one vote for the block, then poll row by row
+      bool pend = false;
 #pragma unroll
-      for (int i = 8 * h; i < 8 * h + 8; ++i)  // Znew rows not yet final: poll
+      for (int i = 8 * h; i < 8 * h + 8; ++i)
         if (k0 + i < cnt && (pks[i] & kNewBit))
-          L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, w[h][i % 8]);
+          pend |= has_sentinel<K, (K % 4 == 0) ? 2 : 1>(w[h][i % 8]);
+      if (__any_sync(kFull, pend)) {
+#pragma unroll
+        for (int i = 8 * h; i < 8 * h + 8; ++i)
+          if (k0 + i < cnt && (pks[i] & kNewBit))
+            L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, w[h][i % 8]);
+      }
       fast_block<KIND, K, MON, ATT>(fp, k0 + 8 * h, cnt, lane, zu, w[h], acc, lsum);
     }
   }
