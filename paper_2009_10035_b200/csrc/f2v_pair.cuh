@@ -27,6 +27,9 @@ constexpr uint32_t kNewBit = 0x80000000u;
 // reader polls the row itself instead of a separate flag (one L2 round trip,
 // no fence on the writer).  Finalised values are never this NaN.
 constexpr uint32_t kSentinel = 0xffc0ffeeu;
+#ifndef F2V_POLL_MAX_NS
+#define F2V_POLL_MAX_NS 256
+#endif
 
 // STEP = 2 for rows written and read as 16-byte vectors (VEC, K % 4 == 0):
 // aligned 8-byte halves are accessed atomically (the assumption NCCL's LL
@@ -100,11 +103,14 @@ struct Lay {
   // polls (minutes) instead of hanging the device.
   __device__ static __forceinline__ void poll(const float* row, int lane, uint32_t d,
                                               float (&v)[K]) {
-    uint32_t it = 0;
+    // exponential back-off (32 ns .. F2V_POLL_MAX_NS): spinning warps would
+    // otherwise take issue slots from the warps streaming rows on the same SM
+    uint32_t it = 0, ns = 32;
     while (__any_sync(kFull, has_sentinel<K, (VEC && K % 4 == 0) ? 2 : 1>(v))) {
-      __nanosleep(20);
+      __nanosleep(ns);
+      ns = ns < F2V_POLL_MAX_NS ? 2 * ns : ns;
       load(row, lane, d, v, true);
-      if (++it == (1u << 28)) __trap();
+      if (++it == (1u << 26)) __trap();
     }
   }
   __device__ static __forceinline__ void store(float* row, int lane, uint32_t d,
