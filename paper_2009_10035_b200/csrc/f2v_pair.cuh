@@ -677,11 +677,12 @@ __device__ __forceinline__ void rows_lowd(const ForceParams& fp, uint32_t packed
     for (int c = 0; c < kLowD; ++c) b |= __float_as_uint(w[c]) == kSentinel;
     return b && mine && (pk & kNewBit);
   };
-  uint32_t it = 0;
+  uint32_t it = 0, ns = 32;
   while (__any_sync(kFull, pending())) {
-    __nanosleep(20);
+    __nanosleep(ns);
+    ns = ns < F2V_POLL_MAX_NS ? 2 * ns : ns;
     if (pending()) load();
-    if (++it == (1u << 28)) __trap();
+    if (++it == (1u << 26)) __trap();
   }
   float red = 0.f, nrm = 0.f;
 #pragma unroll
