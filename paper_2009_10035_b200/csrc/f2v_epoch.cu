@@ -79,8 +79,9 @@ __global__ void scatter_kernel(const uint32_t* __restrict__ lperm, const uint32_
 }
 
 // Mark the vertices that have a window arc (batch(v) in [batch(u) - W,
-// batch(u))): one warp per E item (its vertex and arc range are resolved), so
-// the step of u is read once per item and one atomic per item sets the flag.
+// batch(u))), over the resolved E items: a warp takes 32 consecutive items;
+// items of <= 32 arcs are scanned lane-locally (one item per lane), longer
+// ones by the whole warp; one atomic per item that has a window arc.
 __global__ void window_scan_kernel(const ep::EItem* __restrict__ items,
                                    const uint32_t* __restrict__ n_items,
                                    const uint32_t* __restrict__ col,
@@ -89,15 +90,39 @@ __global__ void window_scan_kernel(const ep::EItem* __restrict__ items,
   const int lane = threadIdx.x & 31;
   const uint32_t total = *n_items;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t it = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < total; it += nw) {
-    const ep::EItem item = items[it];
-    const uint32_t j = __ldg(state + item.u) >> 1;
-    bool win = false;
-    for (uint32_t t = lane; t < item.cnt; t += 32) {
-      const uint32_t bv = __ldg(state + __ldg(col + item.e0 + t)) >> 1;
-      win |= bv < j && bv + W >= j;
+  for (uint32_t base = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; base < total;
+       base += nw * 32) {
+    const uint32_t it = base + lane;
+    const bool valid = it < total;
+    ep::EItem item{};
+    uint32_t j = 0;
+    if (valid) {
+      item = items[it];
+      j = __ldg(state + item.u) >> 1;
     }
-    if (__any_sync(0xffffffffu, win) && lane == 0) atomicOr(wtot + item.u, 1u);
+    if (valid && item.cnt <= 32) {  // lane-local
+      bool win = false;
+      for (uint32_t t = 0; t < item.cnt; ++t) {
+        const uint32_t bv = __ldg(state + __ldg(col + item.e0 + t)) >> 1;
+        win |= bv < j && bv + W >= j;
+      }
+      if (win) atomicOr(wtot + item.u, 1u);
+    }
+    uint32_t big = __ballot_sync(0xffffffffu, valid && item.cnt > 32);
+    while (big) {  // warp-cooperative
+      const int src = __ffs(big) - 1;
+      big &= big - 1;
+      const uint32_t u = __shfl_sync(0xffffffffu, item.u, src);
+      const uint32_t cnt = __shfl_sync(0xffffffffu, item.cnt, src);
+      const uint32_t jj = __shfl_sync(0xffffffffu, j, src);
+      const uint64_t e0 = __shfl_sync(0xffffffffu, item.e0, src);
+      bool win = false;
+      for (uint32_t t = lane; t < cnt; t += 32) {
+        const uint32_t bv = __ldg(state + __ldg(col + e0 + t)) >> 1;
+        win |= bv < jj && bv + W >= jj;
+      }
+      if (__any_sync(0xffffffffu, win) && lane == 0) atomicOr(wtot + u, 1u);
+    }
   }
 }
 
