@@ -105,10 +105,37 @@ class ClockSampler:
     def __init__(self, device):
         self.device = device
         self.samples = []
+        self.source = "nvidia-smi"
+        self.nvml = None
+        try:  # initialised before the timed region starts
+            import pynvml as N
+            N.nvmlInit()
+            self.nvml = (N, N.nvmlDeviceGetHandleByIndex(device))
+        except Exception:
+            self.nvml = None
         self.stop = threading.Event()
         self.th = threading.Thread(target=self.run, daemon=True)
 
     def run(self):
+        # NVML (microsecond queries, sampled every 5 ms) when available, so a
+        # short timed region still gets many samples; nvidia-smi otherwise
+        try:
+            N, h = self.nvml
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            bits = [N.nvmlClocksThrottleReasonHwSlowdown,
+                    N.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    N.nvmlClocksThrottleReasonSwThermalSlowdown,
+                    N.nvmlClocksThrottleReasonSwPowerCap]
+            while not self.stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append([str(sm), str(mx)] +
+                                    ["Active" if r & b else "Not Active" for b in bits])
+                self.stop.wait(0.002)
+            self.source = "nvml"
+            return
+        except Exception:
+            pass
         while not self.stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.device),
@@ -138,7 +165,7 @@ class ClockSampler:
                           if len(s) > 2 + i and s[2 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "source": self.source}
 
 
 def ncu_traffic(cfg_name):
