@@ -568,3 +568,26 @@ def test_full_size_config3_epoch_parity(f2v, orc, dev):
         else:
             z_parity(z, zr)
             assert abs(losses[0] - lr_[0]) <= 1e-9 * abs(lr_[0])
+
+
+@pytest.mark.slow
+def test_full_size_config2_loss_trajectory(f2v, orc, dev):
+    """BASELINE config 2's whole 5-epoch schedule at full size, run
+    independently on both sides from the same U(-1,1) Z: the epoch-loss
+    trajectory agrees within 1e-3 (north_star) and the final Z closely."""
+    g = f2v.rmat_graph(20, 16, seed=1)
+    n = g.num_vertices()
+    dev.upload_graph(g)
+    dev.uniform_embedding(n, 128, 1)
+    z0 = dev.get_embedding()
+    cfg = f2v.TrainConfig(dim=128, batch=384, negatives=5, lr=0.02, epochs=5,
+                          model=kind_model(f2v, "tdist"), seed=1, monitor_loss=True,
+                          sampler="philox")
+    losses = dev.train_epochs(cfg)
+    z = dev.get_embedding()
+    rc, zr, lr_, _, _ = orc.orc_train(g.row_offsets, g.col_indices, z0, 384, 5, 0.02, 5, "tdist",
+                                      1, sampler="philox", threads=os.cpu_count() or 8)
+    assert rc == 0
+    np.testing.assert_allclose(losses, lr_, rtol=1e-3)
+    rel = np.linalg.norm(z.astype(np.float64) - zr) / np.linalg.norm(zr)
+    assert rel < 1e-4, rel
