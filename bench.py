@@ -3,25 +3,33 @@
 edge+neg-sample updates/s and sec/epoch at d=128; % of HBM roofline).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config c2|c1|c3|c4]
+                    [--config c3|c1|c2|c4|c5] [--precision exact|fast]
 
 A "step" is one epoch of train() (trainer.cpp:211-249) over the whole graph:
-every batch's fused gradient + update.  Default workload = BASELINE config 2
-(R-MAT scale 20, edge factor 16, (.57,.19,.19,.05), symmetrised/deduplicated,
-t-distribution, d=128, b=384, s=5, lr=.02, 5-epoch schedule, Philox
-negatives, Z ~ U(-1,1)), synthetic (no dataset).
+every batch's fused gradient + update.  Default workload = BASELINE config 3,
+the config north_star's target names (Chung-Lu n=3M power-law graph, 230M
+directed arcs, sigmoid, d=128, b=384, s=5, lr=.02, Philox negatives,
+Z ~ U(-1,1)), synthetic (no dataset), at the reference's arithmetic
+(precision="exact": fp64 pair math and accumulation in the reference's order).
 
 Printed JSON (rank 0, one line):
   value  = (nnz + n*s) * K / (device time of K epochs), inputs resident in HBM,
            timed with CUDA events on the library's stream;
+  fast   = the same K epochs with precision="fast" (fp32 pair math, fp64
+           accumulation) -- reported beside the headline, not as it;
   e2e    = same metric through the public API with host buffers: per step one
-           full train() of the config (5 epochs) including H2D of CSR + Z from
-           pinned memory and D2H of Z;
+           full train() of the config's epoch schedule including H2D of CSR + Z
+           from pinned memory and D2H of Z;
   roofline = algorithmic bytes per epoch-kernel launch / its event-timed
            duration vs MEASURED_PEAKS.json hbm_gbs; traffic from the committed
-           ncu capture (profiles/) when it matches the config;
+           ncu capture (profiles/ncu_traffic.json) of the same config+precision;
   cpu_baseline = the unmodified reference (oracle/_ref) on this host's cores
            over a bounded sample of batches.
+
+--impl reference never loads the product library: the oracle's restated
+generator emits the edge list, the reference's own from_edges builds the CSR
+(once per process), and the reference core times a bounded sample of epoch 0
+with the same Philox negatives the device draws.
 """
 from __future__ import annotations
 
@@ -180,57 +188,94 @@ def ncu_traffic(cfg_name):
         return None
 
 
-def reference_cpu(g, z0, cfg_name, budget_s=20.0, workers=None, sample_batches=None):
-    """The unmodified reference core (oracle/_ref) on this host's cores, over a
-    bounded prefix of epoch 0's batches: partition_epoch + build_minibatch +
-    make_schedule + grad_minibatch + apply_update (trainer.cpp:210-236)."""
-    import ctypes as C
+def philox_negs(n, b, s, nb, epoch=0, seed=1):
+    """The configs' Philox negatives of batches 0..nb-1 of one epoch (the same
+    stream the device samples), from the oracle's restatement."""
     import pyoracle as P
+    out = np.zeros(nb * s, np.uint32)
+    for bi in range(nb):
+        out[bi * s:(bi + 1) * s] = P.orc_negatives("philox", seed, epoch, bi, n, s)
+    return out
 
-    _, _, kind, d, b, s, lr, _ = CONFIGS[cfg_name]
-    kind_id = P.KINDS[kind]
-    n = g.num_vertices()
-    workers = workers or os.cpu_count()
-    kindname = "reference"
+
+def reference_graph(cfg_name):
+    """The config's graph built without the product library: the oracle's
+    restated generator (oracle/f2v_oracle_gen.c) emits the edge list, the
+    reference's own CsrGraph::from_edges (csr_graph.cpp:57-97, oracle/_ref)
+    builds the CSR.  Returns ("reference", RefGraph, n, nnz), or ("port",
+    (rowptr, col), n, nnz) with the C restatement when _ref is absent."""
+    import pyoracle as P
+    gen, kw, *_ = CONFIGS[cfg_name]
+    t0 = time.perf_counter()
+    pairs, n = P.orc_gen_pairs(gen, **kw)
+    t1 = time.perf_counter()
     if P.reference_available():
-        R = P.reference()
-        t0 = time.perf_counter()
-        rg = P.RefGraph.from_csr(g.row_offsets, g.col_indices)
-        log(f"reference CsrGraph::from_edges: {time.perf_counter() - t0:.1f}s")
+        rg = P.ref_graph_from_edges(pairs, n, True)
+        del pairs
+        nnz = P.reference().ref_graph_nnz(rg.ptr)
+        log(f"graph {cfg_name} (oracle edge list {t1 - t0:.1f}s, reference from_edges "
+            f"{time.perf_counter() - t1:.1f}s): n={n} nnz={nnz}")
+        return "reference", rg, n, nnz
+    rowptr, col, _, _ = P.orc_from_edges(pairs, n, True)
+    log(f"graph {cfg_name} (oracle edge list + C restatement of from_edges "
+        f"{time.perf_counter() - t0:.1f}s): n={n} nnz={len(col)}")
+    return "port", (rowptr, col), n, len(col)
 
-        def run(nb):
+
+class ReferenceCPU:
+    """The reference's CPU path on this host's cores over a bounded prefix of
+    epoch 0's batches: partition_epoch + build_minibatch (Philox negatives
+    injected, as the device draws them) + make_schedule + grad_minibatch +
+    apply_update (trainer.cpp:210-236), monitoring off.  kind "reference" =
+    the unmodified reference core (oracle/_ref); "port" = the C restatement."""
+
+    def __init__(self, kind, graph, n, z0, cfg_name, workers=None):
+        import pyoracle as P
+        _, _, fkind, d, b, s, lr, _ = CONFIGS[cfg_name]
+        self.P, self.kind, self.graph, self.n, self.z0 = P, kind, graph, n, z0
+        self.fkind, self.d, self.b, self.s, self.lr = fkind, d, min(b, n), s, lr
+        self.workers = workers or os.cpu_count()
+        self.nb_total = (n + self.b - 1) // self.b
+        self.negs = philox_negs(n, self.b, s, self.nb_total)
+        if kind == "port":
+            self.perm = P.orc_epoch_perm(n, self.b, 1, 0)
+
+    def run(self, nb):
+        import ctypes as C
+        P = self.P
+        z = np.array(self.z0, copy=True)
+        if self.kind == "reference":
             pairs = C.c_uint64()
-            z = np.array(z0, copy=True)
-            secs = R.ref_time_batches(rg.ptr, z, d, b, s, np.float32(lr), kind_id, 1, workers, nb,
-                                      C.byref(pairs))
+            secs = P.reference().ref_time_batches(
+                self.graph.ptr, z, self.d, self.b, self.s, np.float32(self.lr),
+                P.KINDS[self.fkind], 1, self.workers, nb, self.negs.ctypes.data_as(C.c_void_p),
+                C.byref(pairs))
             return secs, pairs.value
-    else:  # the C restatement (single-threaded port per batch, pthreads per batch)
-        kindname = "port"
-        O = P.oracle()
-        perm = P.orc_epoch_perm(n, min(b, n), 1, 0)
+        rowptr, col = self.graph
+        t0 = time.perf_counter()
+        pairs = 0
+        for bi in range(nb):
+            ids = self.perm[bi * self.b:(bi + 1) * self.b]
+            negs = self.negs[bi * self.s:(bi + 1) * self.s]
+            rc, grads, _ = P.orc_grad_minibatch(rowptr, col, z, ids, negs, self.fkind,
+                                                threads=self.workers)
+            P.oracle().orc_apply_update(z, self.d, ids, len(ids), grads, np.float32(self.lr))
+            pairs += int((rowptr[ids + 1] - rowptr[ids]).sum()) + len(ids) * self.s
+        return time.perf_counter() - t0, pairs
 
-        def run(nb):
-            z = np.array(z0, copy=True)
-            t0 = time.perf_counter()
-            pairs = 0
-            for bi in range(nb):
-                ids = perm[bi * b:(bi + 1) * b]
-                negs = P.orc_negatives("philox", 1, 0, bi, n, s)
-                rc, grads, _ = P.orc_grad_minibatch(g.row_offsets, g.col_indices, z, ids, negs,
-                                                    kind, threads=workers)
-                O.orc_apply_update(z, d, ids, len(ids), grads, np.float32(lr))
-                pairs += int((g.row_offsets[ids + 1] - g.row_offsets[ids]).sum()) + len(ids) * s
-            return time.perf_counter() - t0, pairs
-    nb_total = (n + b - 1) // b
-    if sample_batches is None:
-        probe = min(nb_total, 16)
-        secs, _ = run(probe)
-        sample_batches = int(min(nb_total, max(probe, probe * budget_s / max(secs, 1e-6))))
-    secs, pairs = run(sample_batches)
-    return {"value": pairs / secs, "unit": "updates/s", "cores": workers, "kind": kindname,
-            "sample": f"first {sample_batches} of {nb_total} batches of epoch 0 "
-                      f"({pairs} pair updates, {secs:.1f}s, {workers} worker threads)",
-            "sec_per_epoch_extrapolated": secs * nb_total / sample_batches}
+    def size_for(self, budget_s):
+        probe = min(self.nb_total, 16)
+        secs, _ = self.run(probe)
+        return int(min(self.nb_total, max(probe, probe * budget_s / max(secs, 1e-6))))
+
+    def measure(self, nb):
+        secs, pairs = self.run(nb)
+        return {"value": pairs / secs, "unit": "updates/s", "cores": self.workers,
+                "kind": self.kind,
+                "sample": f"first {nb} of {self.nb_total} batches of epoch 0 ({pairs} pair "
+                          f"updates, {secs:.1f}s, {self.workers} worker threads, Philox "
+                          f"negatives injected)",
+                "sec_per_epoch_extrapolated": secs * self.nb_total / nb}
 
 
 def dist_env():
@@ -240,44 +285,96 @@ def dist_env():
     return rank, world, local
 
 
+def config_block(cfg_name, n, nnz, world):
+    """`config` of both arms (identical keys and values for the same run)."""
+    gen, kw, kind, d, b, s, lr, epochs = CONFIGS[cfg_name]
+    return {"workload": WORKLOAD_NAMES[cfg_name], "config_id": cfg_name, "n": n, "nnz": nnz,
+            "dim": d, "batch": b, "negatives": s, "lr": lr, "force_model": kind,
+            "epochs_schedule": epochs, "sampler": "philox", "init": "U(-1,1) from Rng(1, 0)",
+            "arithmetic": "fp64 pair math and accumulation (the reference's operation order), "
+                          "fp32 Z",
+            "parallelism": f"vertex shards x{world}" if world > 1 else "1 GPU",
+            "step": "one epoch (all batches) of train()"}
+
+
 def bench_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    import paper_2009_10035_b200 as f2v
+    import pyoracle as P
 
     cfg_name = args.config
     _, _, kind, d, b, s, lr, epochs = CONFIGS[cfg_name]
-    g = make_graph(f2v, cfg_name)
-    n = g.num_vertices()
-    import pyoracle as P
+    rkind, graph, n, nnz = reference_graph(cfg_name)
     z0 = np.zeros((n, d), np.float32)
-    P.oracle().orc_random_embedding(n, d, 1, z0)
-    # per step: a bounded sample of the same workload (budget split over steps)
-    per_step = max(3.0, min(20.0, 120.0 / max(1, args.steps + args.warmup)))
-    first = reference_cpu(g, z0, cfg_name, budget_s=per_step)
-    nb = int(first["sample"].split()[1])
-    vals = [first["value"]]
-    for _ in range(max(0, args.steps - 1)):
-        vals.append(reference_cpu(g, z0, cfg_name, sample_batches=nb)["value"])
-    v = float(np.median(vals))
-    nnz = g.num_edges()
+    P.oracle().orc_random_embedding(n, d, 1, z0)  # U(-1,1) from Rng(1, 0), A.5
+    ref = ReferenceCPU(rkind, graph, n, z0, cfg_name)
+    # each step: a bounded sample of the epoch (the whole run within minutes)
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    nb = ref.size_for(per_step)
+    for _ in range(args.warmup):  # untimed warm-up samples (a few batches each)
+        ref.run(min(nb, 4))
+    runs = [ref.measure(nb) for _ in range(max(1, args.steps))]
+    v = float(np.median([r["value"] for r in runs]))
+    pairs = nnz + n * s
     out = {
         "impl": "reference", "metric": "edge+neg-sample updates/sec (d=128)" if d == 128 else
         "edge+neg-sample updates/sec", "value": v, "unit": "updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * (nnz + n * s) / v, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * pairs / v, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_NAMES[cfg_name], "n": n, "nnz": nnz, "batch": b,
-                   "negatives": s, "epoch_sample": first["sample"]},
-        "sec_per_epoch": (nnz + n * s) / v,
-        "cpu_baseline": {k: first[k] for k in ("cores", "kind", "sample")} | {"value": v,
-                                                                             "unit": "updates/s"},
+        "config": config_block(cfg_name, n, nnz, 1),
+        "sec_per_epoch": pairs / v,
+        "cpu_baseline": {k: runs[0][k] for k in ("cores", "kind", "sample")} | {
+            "value": v, "unit": "updates/s"},
         "e2e": {"value": v, "unit": "updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
     return 0
+
+
+def timed_epochs(f2v, dev, cfg, args, local, world):
+    """K device-resident epochs in one train_epochs call after W warm-up
+    epochs; CUDA events on the library stream (max over ranks)."""
+    dev.train_epochs(cfg, 0, args.warmup)  # untimed warm-up epochs
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    f2v._lib.f2v_kernel_launches(dev._h, 1)
+    with ClockSampler(local) as clk:
+        t_wall = time.perf_counter()
+        dev.train_epochs(cfg, args.warmup, args.steps)  # K timed epochs, one call
+        t_wall = time.perf_counter() - t_wall
+    t = dev.last_timing()
+    dev_ms, kern_ms, nk = t["device_ms"], t["epoch_kernel_ms"], t["epoch_kernels"]
+    assert nk == args.steps, (nk, args.steps)
+    launches = f2v._lib.f2v_kernel_launches(dev._h, 0)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        tt = torch.tensor([dev_ms, kern_ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dev_ms, kern_ms = float(tt[0].item()), float(tt[1].item())
+    return dev_ms, kern_ms, nk, launches, clk.summary(), t_wall
+
+
+def roofline(cfg_name, precision, n, nnz, d, b, s, kern_ms_per_launch, world):
+    algo = algorithmic_bytes(n, nnz, d, min(b, n), s)
+    peak, peak_kind = hbm_peak()
+    achieved = algo / (kern_ms_per_launch / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
+            "frac": achieved / (peak * world),
+            "traffic": ncu_traffic(f"{cfg_name}_{precision}") if world == 1 else None,
+            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" + (
+                f" x {world} GPUs" if world > 1 else "") if peak_kind == "measured"
+            else "fallback 6650 GB/s (B200_PROFILING.md)",
+            "algorithmic_bytes_per_launch": algo,
+            "kernel_ms_per_launch": kern_ms_per_launch}
+
+
+PRECISION_DTYPE = {"exact": "f64",  # fp64 pair math + accumulation, as the reference
+                   "fast": "f32 pair math / f64 accumulate"}
 
 
 def bench_b200(args):
@@ -298,7 +395,7 @@ def bench_b200(args):
     cfg = f2v.TrainConfig(dim=d, batch=b, negatives=s, lr=lr,
                           epochs=args.warmup + args.steps,
                           model=f2v.ForceModel(f2v.ForceKind.parse(kind)), seed=1,
-                          monitor_loss=False, sampler="philox")
+                          monitor_loss=False, sampler="philox", precision=args.precision)
     # F2V_BENCH_SHARDED=1 runs the sharded code path at world 1 as well
     sharded = world > 1 or bool(os.environ.get("F2V_BENCH_SHARDED"))
     if sharded:
@@ -314,47 +411,32 @@ def bench_b200(args):
         dev = f2v.Device(local)
         dev.upload_graph(g)
         dev.uniform_embedding(n, d, 1, -1.0, 1.0)  # the configs' U(-1,1) from Rng(seed, 0)
-    dev.train_epochs(cfg, 0, args.warmup)  # untimed warm-up epochs
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
-    f2v._lib.f2v_kernel_launches(dev._h, 1)
-    with ClockSampler(local) as clk:
-        t_wall = time.perf_counter()
-        dev.train_epochs(cfg, args.warmup, args.steps)  # K timed epochs, one call
-        t_wall = time.perf_counter() - t_wall
-    t = dev.last_timing()
-    dev_ms, kern_ms, nk = t["device_ms"], t["epoch_kernel_ms"], t["epoch_kernels"]
-    assert nk == args.steps
-    launches = f2v._lib.f2v_kernel_launches(dev._h, 0)
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        tt = torch.tensor([dev_ms, kern_ms], device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dev_ms, kern_ms = float(tt[0].item()), float(tt[1].item())
+    z_start = dev.get_embedding() if args.precision == "exact" and not args.no_fast else None
+    dev_ms, kern_ms, nk, launches, clocks, t_wall = timed_epochs(f2v, dev, cfg, args, local,
+                                                                 world)
     z = dev.get_embedding()
     assert np.all(np.isfinite(z)), "non-finite embedding"
     pairs = nnz + n * s
     # the G shards split ONE epoch of the whole graph: total work is fixed
     value = pairs * args.steps / (dev_ms / 1e3)
     ms_per_step = dev_ms / args.steps
-    algo = algorithmic_bytes(n, nnz, d, min(b, n), s)
-    peak, peak_kind = hbm_peak()
-    achieved = algo / (kern_ms / nk / 1e3) / 1e9
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak * world, "unit": "GB/s",
-            "frac": achieved / (peak * world), "traffic": ncu_traffic(cfg_name) if world == 1
-            else None,
-            "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" + (
-                f" x {world} GPUs" if world > 1 else "") if peak_kind == "measured"
-            else "fallback 6650 GB/s (B200_PROFILING.md)",
-            "algorithmic_bytes_per_launch": algo,
-            "kernel_ms_per_launch": kern_ms / nk}
+    roof = roofline(cfg_name, args.precision, n, nnz, d, b, s, kern_ms / nk, world)
     if world > 1:  # the fused row exchange: every GPU stores its rows into G-1 replicas
         xbytes = (world - 1) * (n // world) * 4 * d
         roof["nvlink"] = {"bytes_per_gpu_per_epoch": xbytes,
                           "achieved_GBps": xbytes / (kern_ms / nk / 1e3) / 1e9,
                           "peak_GBps": 900.0, "peak_source": "NVLink 5 nominal per direction"}
+    fast = None
+    if z_start is not None:  # the same epochs with fp32 pair math (precision="fast")
+        dev.set_embedding(z_start) if not sharded else None
+        cfg_f = dataclasses.replace(cfg, precision="fast")
+        f_ms, f_kms, f_nk, _, f_clk, _ = timed_epochs(f2v, dev, cfg_f, args, local, world)
+        fast = {"value": pairs * args.steps / (f_ms / 1e3), "unit": "updates/s",
+                "ms_per_step": f_ms / args.steps, "dtype": PRECISION_DTYPE["fast"],
+                "roofline": roofline(cfg_name, "fast", n, nnz, d, b, s, f_kms / f_nk, world),
+                "clocks": f_clk,
+                "note": "precision='fast': fp32 dot/distance and force term, fp32 8-pair "
+                        "block sums, fp64 per-vertex accumulation; not the headline"}
     # ------------------------------------------------------------ e2e
     import torch
     h_row = torch.from_numpy(g.row_offsets).pin_memory().numpy()
@@ -367,7 +449,8 @@ def bench_b200(args):
     g_pinned = f2v.CsrGraph(h_row, h_col)
 
     cfg_e2e = f2v.TrainConfig(dim=d, batch=b, negatives=s, lr=lr, epochs=epochs,
-                              model=cfg.model, seed=1, monitor_loss=False, sampler="philox")
+                              model=cfg.model, seed=1, monitor_loss=False, sampler="philox",
+                              precision=args.precision)
 
     if sharded:
         cfg_e2e = dataclasses.replace(cfg_e2e, shards=world)
@@ -399,38 +482,45 @@ def bench_b200(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e_val = pairs * epochs / e2e_s
-    h2d = h_row.nbytes + h_col.nbytes + h_z0.nbytes + 4 * n * epochs  # + perms
+    h2d = h_row.nbytes + h_col.nbytes + h_z0.nbytes
     d2h = h_z.nbytes
     dev.close()
     if rank != 0:
         return 0
+    conf = config_block(cfg_name, n, nnz, world)
+    if args.precision != "exact":
+        conf["arithmetic"] = PRECISION_DTYPE[args.precision]
+    conf["l2"] = "inputs larger than L2 (Z 2x%d MB + CSR %d MB > 126 MB)" % (
+        n * d * 4 >> 20, (nnz * 4 + n * 8) >> 20)
     out = {
         "metric": "edge+neg-sample updates/sec (d=128)" if d == 128 else
         "edge+neg-sample updates/sec", "value": value, "unit": "updates/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_NAMES[cfg_name], "n": n, "nnz": nnz, "batch": b,
-                   "negatives": s, "epochs_schedule": epochs, "sampler": "philox",
-                   "parallelism": f"vertex-partitioned shards x{world} (NVLink row stores)"
-                   if world > 1 else "1 GPU",
-                   "step": "one epoch (all batches) of train()",
-                   "l2": "inputs larger than L2 (Z 2x%d MB + CSR %d MB > 126 MB)" %
-                         (n * d * 4 >> 20, (nnz * 4 + n * 8) >> 20)},
+        "vs_baseline": None, "dtype": PRECISION_DTYPE[args.precision], "data": "synthetic",
+        "config": conf,
         "sec_per_epoch": ms_per_step / 1e3,
         "roofline": roof,
         "e2e": {"value": e2e_val, "unit": "updates/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "step": f"one train() of the {epochs}-epoch schedule via the public API "
-                        f"(host CSR+Z in from pinned memory, Z out): {e2e_s * 1e3:.1f} ms"},
+                        f"(CSR + Z copied in from pinned host buffers the bench allocates, "
+                        f"Z copied out): {e2e_s * 1e3:.1f} ms"},
         "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "clocks": clocks,
         "wall_s_timed_region": t_wall,
     }
+    if fast is not None:
+        out["fast"] = fast
     if world == 1 and not args.no_cpu_baseline:
-        z0 = h_z0
         try:
-            out["cpu_baseline"] = reference_cpu(g, z0, cfg_name, budget_s=args.cpu_budget)
+            import pyoracle as P
+            if P.reference_available():
+                graph, rk = P.RefGraph.from_csr(g.row_offsets, g.col_indices), "reference"
+            else:
+                graph, rk = (g.row_offsets, g.col_indices), "port"
+            ref = ReferenceCPU(rk, graph, n, h_z0, cfg_name)
+            out["cpu_baseline"] = ref.measure(ref.size_for(args.cpu_budget))
         except Exception as ex:  # reported, not hidden
             out["cpu_baseline"] = {"value": None, "error": str(ex)}
     print(json.dumps(out), flush=True)
@@ -443,9 +533,11 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default="exact", choices=["exact", "fast"])
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fast", action="store_true", help="skip the precision='fast' run")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         log("note: warm-up raised to the contract minimum of 3")

@@ -56,7 +56,9 @@ extern "C" {
 typedef struct {
   int32_t kind;          /* F2V_SIGMOID .. F2V_LINLOG */
   float epsilon;         /* singularity clamp, default 1e-6f */
-  float repulsion_cap;   /* <= 0: std::nullopt (no clamp); default 5.0f */
+  float repulsion_cap;   /* the clamp value when has_repulsion_cap (any value, as the
+                            reference's std::optional<float>: 0 zeroes repulsion) */
+  int32_t has_repulsion_cap; /* 0: std::nullopt (no clamp); default 1 with 5.0f */
 } f2v_force_model;
 
 /* TrainConfig, trainer.hpp:15-30 (+ the device-side fields of SURVEY §8b) */

@@ -203,7 +203,7 @@ static void scaled_unit_diff(double scalar, const float* zu, const float* zo, do
     out[i] = scalar * ((double)zu[i] - (double)zo[i]) / t;
 }
 static void clamp_magnitude(float capf, double magnitude, uint32_t d, double* out) {
-  if (!(capf > 0)) return; /* repulsion_cap unset */
+  if (isnan(capf)) return; /* repulsion_cap unset (std::nullopt); 0 still clamps */
   const double cap = (double)capf;
   if (magnitude <= cap || magnitude == 0.0) return;
   const double scale = cap / magnitude;

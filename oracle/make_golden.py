@@ -158,12 +158,13 @@ def gen_pair(R):
         zu = np.ascontiguousarray(zu, np.float32)
         zo = np.ascontiguousarray(zo, np.float32)
         out = np.zeros(d, np.float64)
-        rc = R.ref_pair_grad(kind, eps, cap, zu, zo, d, att, out)
+        rcap = float("nan") if cap < 0 else cap  # -1 in the fixture = std::nullopt
+        rc = R.ref_pair_grad(kind, eps, rcap, zu, zo, d, att, out)
         o32 = np.zeros(d, np.float32)
-        R.ref_pair_grad_f32(kind, eps, cap, zu, zo, d, att, o32)
+        R.ref_pair_grad_f32(kind, eps, rcap, zu, zo, d, att, o32)
         lv = C.c_double(np.nan)
         if kind in (0, 1):
-            R.ref_pair_loss(kind, eps, cap, zu, zo, d, att, C.byref(lv))
+            R.ref_pair_loss(kind, eps, rcap, zu, zo, d, att, C.byref(lv))
         zu_l.append(zu); zo_l.append(zo); gout.append(out); gf32.append(o32)
         lout.append(lv.value)
         meta.append((kind, att, d, rc, eps, cap))

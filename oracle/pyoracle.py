@@ -64,6 +64,12 @@ def oracle():
                                           C.POINTER(C.c_uint64)])
         _sig(L, "orc_sbm_edges", C.c_uint64, [C.c_uint32, C.c_int, C.c_double, C.c_double,
                                             C.c_uint64, u32p, C.c_uint64])
+        _sig(L, "orc_gen_rmat", C.c_uint64, [C.c_uint32, C.c_uint32, C.c_double, C.c_double,
+                                           C.c_double, C.c_uint64, C.c_void_p])
+        _sig(L, "orc_gen_chung_lu", C.c_uint64, [C.c_uint32, C.c_double, C.c_double, C.c_double,
+                                               C.c_double, C.c_uint64, C.c_void_p])
+        _sig(L, "orc_gen_rgg", C.c_uint64, [C.c_uint32, C.c_double, C.c_uint64, C.c_void_p,
+                                          C.c_uint64])
         _sig(L, "orc_stable_sigmoid", C.c_double, [C.c_double])
         _sig(L, "orc_pair_grad", C.c_int, [C.c_int, C.c_float, C.c_float, f32p, f32p, C.c_uint32,
                                          C.c_int, f64p])
@@ -157,7 +163,8 @@ def reference():
                                            C.c_uint32, C.c_int, f32p, f64p])
         _sig(L, "ref_time_batches", C.c_double, [C.c_void_p, f32p, C.c_uint32, C.c_uint32,
                                                C.c_uint32, C.c_float, C.c_int, C.c_uint64,
-                                               C.c_uint32, C.c_uint64, C.POINTER(C.c_uint64)])
+                                               C.c_uint32, C.c_uint64, C.c_void_p,
+                                               C.POINTER(C.c_uint64)])
         _sig(L, "ref_hardware_threads", C.c_uint, [])
         _ref = L
     return _ref
@@ -197,6 +204,13 @@ class RefGraph:
             np.ascontiguousarray(col if len(col) else np.zeros(1, np.uint32), np.uint32)))
 
 
+def capv(cap):
+    """repulsion_cap as the oracle/driver take it: None -> NaN (std::nullopt);
+    any other value clamps (0 included).  The golden fixtures written by
+    make_golden.py encode an unset cap as -1."""
+    return float("nan") if cap is None else float(cap)
+
+
 def orc_from_edges(pairs, n, symmetrize=True):
     """C restatement of CsrGraph::from_edges -> (rowptr, col, dups, loops)."""
     L = oracle()
@@ -219,6 +233,46 @@ def orc_sbm_graph(n, blocks, p_in, p_out, seed):
     pairs = np.zeros(2 * max(m, 1), np.uint32)
     L.orc_sbm_edges(n, blocks, p_in, p_out, seed, pairs, m)
     return orc_from_edges(pairs[: 2 * m], n, True)[:2]
+
+
+def orc_gen_pairs(gen, **kw):
+    """The configs' synthetic edge list (uint32 [m, 2]) from oracle/f2v_oracle_gen.c."""
+    L = oracle()
+    if gen == "sbm":
+        n = kw["n"]
+        m = L.orc_sbm_edges(n, kw["blocks"], kw["p_in"], kw["p_out"], kw["seed"],
+                            np.zeros(2, np.uint32), 0)
+        pairs = np.zeros(2 * max(m, 1), np.uint32)
+        L.orc_sbm_edges(n, kw["blocks"], kw["p_in"], kw["p_out"], kw["seed"], pairs, m)
+        return pairs[: 2 * m].reshape(-1, 2), n
+    if gen == "rmat":
+        args = (kw["scale"], kw["edge_factor"], kw["a"], kw["b"], kw["c"], kw["seed"])
+        m = L.orc_gen_rmat(*args, None)
+        pairs = np.zeros(2 * m, np.uint32)
+        L.orc_gen_rmat(*args, pairs.ctypes.data_as(C.c_void_p))
+        return pairs.reshape(-1, 2), 1 << kw["scale"]
+    if gen == "chung_lu":
+        args = (kw["n"], kw["exponent"], kw["min_deg"], kw["max_deg"], kw["mean_deg"], kw["seed"])
+        m = L.orc_gen_chung_lu(*args, None)
+        pairs = np.zeros(2 * m, np.uint32)
+        L.orc_gen_chung_lu(*args, pairs.ctypes.data_as(C.c_void_p))
+        return pairs.reshape(-1, 2), kw["n"]
+    if gen == "rgg":
+        m = L.orc_gen_rgg(kw["n"], kw["mean_deg"], kw["seed"], None, 0)
+        pairs = np.zeros(2 * max(m, 1), np.uint32)
+        L.orc_gen_rgg(kw["n"], kw["mean_deg"], kw["seed"], pairs.ctypes.data_as(C.c_void_p), m)
+        return pairs[: 2 * m].reshape(-1, 2), kw["n"]
+    raise ValueError(gen)
+
+
+def ref_graph_from_edges(pairs, n, symmetrize=True):
+    """The reference's own CsrGraph::from_edges (csr_graph.cpp:57-97) -> RefGraph."""
+    pairs = np.ascontiguousarray(pairs, np.uint32).reshape(-1)
+    m = len(pairs) // 2
+    dups, loops = C.c_uint64(), C.c_uint64()
+    return RefGraph(reference().ref_graph_from_edges(pairs if m else np.zeros(2, np.uint32), m,
+                                                     n, int(symmetrize), C.byref(dups),
+                                                     C.byref(loops)))
 
 
 def orc_rng_keyed(seed, key):
@@ -250,7 +304,7 @@ def orc_pair_grad(kind, zu, zo, attractive, eps=1e-6, cap=5.0):
     zu = np.ascontiguousarray(zu, np.float32)
     zo = np.ascontiguousarray(zo, np.float32)
     out = np.zeros(len(zu), np.float64)
-    rc = oracle().orc_pair_grad(KINDS.get(kind, kind), eps, cap, zu, zo, len(zu),
+    rc = oracle().orc_pair_grad(KINDS.get(kind, kind), eps, capv(cap), zu, zo, len(zu),
                                 int(attractive), out)
     if rc:
         raise ValueError("unsupported")
@@ -261,7 +315,7 @@ def orc_pair_loss(kind, zu, zo, attractive, eps=1e-6, cap=5.0):
     zu = np.ascontiguousarray(zu, np.float32)
     zo = np.ascontiguousarray(zo, np.float32)
     out = C.c_double()
-    rc = oracle().orc_pair_loss(KINDS.get(kind, kind), eps, cap, zu, zo, len(zu),
+    rc = oracle().orc_pair_loss(KINDS.get(kind, kind), eps, capv(cap), zu, zo, len(zu),
                                 int(attractive), C.byref(out))
     if rc:
         raise ValueError("unsupported")
@@ -277,7 +331,7 @@ def orc_grad_minibatch(rowptr, col, z, ids, negs, kind, eps=1e-6, cap=5.0, threa
     bad = C.c_uint32(0)
     colc = np.ascontiguousarray(col if len(col) else np.zeros(1, np.uint32), np.uint32)
     rc = oracle().orc_grad_minibatch(np.ascontiguousarray(rowptr, np.uint64), colc, n, z, d, ids,
-                                     len(ids), negs, len(negs), KINDS.get(kind, kind), eps, cap,
+                                     len(ids), negs, len(negs), KINDS.get(kind, kind), eps, capv(cap),
                                      threads, grads, C.byref(bad))
     return rc, grads, bad.value
 
@@ -289,7 +343,7 @@ def orc_batch_loss(rowptr, col, z, ids, negs, kind, eps=1e-6, cap=5.0):
     rc = oracle().orc_batch_loss(np.ascontiguousarray(rowptr, np.uint64), colc, z, z.shape[1],
                                  np.ascontiguousarray(ids, np.uint32), len(ids),
                                  np.ascontiguousarray(negs, np.uint32), len(negs),
-                                 KINDS.get(kind, kind), eps, cap, C.byref(out))
+                                 KINDS.get(kind, kind), eps, capv(cap), C.byref(out))
     if rc:
         raise ValueError("unsupported")
     return out.value
@@ -313,7 +367,7 @@ def orc_train(rowptr, col, z0, batch, s, lr, epochs, kind, seed, eps=1e-6, cap=5
         cb = STEP_CB()
     colc = np.ascontiguousarray(col if len(col) else np.zeros(1, np.uint32), np.uint32)
     rc = oracle().orc_train_mode(np.ascontiguousarray(rowptr, np.uint64), colc, n, z, d, batch,
-                                 s, lr, epochs, KINDS.get(kind, kind), eps, cap, seed,
+                                 s, lr, epochs, KINDS.get(kind, kind), eps, capv(cap), seed,
                                  int(lr_decay), int(monitor), 1 if sampler in ("philox", 1) else 0,
                                  G, walk, threads, losses, counters, cb, None, fail)
     return rc, z, losses, counters, fail

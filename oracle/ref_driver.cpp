@@ -16,6 +16,7 @@
 //   * the train() loop of trainer.cpp:192-251 with an injected initial Z and
 //     (optionally) injected negatives, as SURVEY.md §8(c) prescribes.
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <numeric>
@@ -39,7 +40,8 @@ ForceModel make_model(int kind, float eps, float cap) {
   ForceModel m;
   m.kind = static_cast<ForceKind>(kind);
   m.epsilon = eps;
-  if (cap > 0) m.repulsion_cap = cap; else m.repulsion_cap.reset();
+  // NaN = std::nullopt; any other value is a cap (0 zeroes the repulsion)
+  if (!std::isnan(cap)) m.repulsion_cap = cap; else m.repulsion_cap.reset();
   return m;
 }
 
@@ -414,11 +416,14 @@ int ref_train_stock(void* gp, std::uint32_t d, std::uint32_t batch, std::uint32_
 // CPU baseline timer: the timed region of train() (trainer.cpp:210-236) --
 // partition_epoch + build_minibatch + make_schedule + grad_minibatch +
 // apply_update -- for the first `max_batches` batches of epoch 0, monitoring
-// off.  Returns seconds; pairs_out = attractive + repulsive evaluations.
+// off.  negs_in == nullptr: build_minibatch's own negatives; otherwise batch
+// bi's s negatives are negs_in[bi*s ..] (the BASELINE configs' Philox stream,
+// injected into the Minibatch exactly as ref_train does).  Returns seconds;
+// pairs_out = attractive + repulsive evaluations.
 double ref_time_batches(void* gp, float* z, std::uint32_t d, std::uint32_t batch,
                         std::uint32_t s, float lr, int kind, std::uint64_t seed,
                         std::uint32_t workers, std::uint64_t max_batches,
-                        std::uint64_t* pairs_out) {
+                        const std::uint32_t* negs_in, std::uint64_t* pairs_out) {
   const CsrGraph& g = *static_cast<CsrGraph*>(gp);
   const VertexId n = g.num_vertices();
   const VertexId b = std::min<VertexId>(batch, n);
@@ -435,6 +440,7 @@ double ref_time_batches(void* gp, float* z, std::uint32_t d, std::uint32_t batch
     const auto ids = part.batch(bi);
     Rng batch_rng = Rng::keyed(seed, {0x33, 0u, bi});
     Minibatch mb = build_minibatch(g, ids, SampleMode::one_hop(), s, batch_rng);
+    if (negs_in) mb.negatives.assign(negs_in + bi * s, negs_in + (bi + 1) * s);
     BatchSchedule sched = make_schedule(g, ids, workers, true);
     grad_minibatch(g, zm, mb, model, sched, grads, &tc);
     apply_update(zm, ids, grads, lr);

@@ -75,7 +75,8 @@ _ERRORS = {1: UsageError, 2: IoError, 3: RangeError, 4: NumericalError, 5: CudaE
 
 # ------------------------------------------------------------ C-ABI structs
 class _ForceModel(C.Structure):
-    _fields_ = [("kind", C.c_int32), ("epsilon", C.c_float), ("repulsion_cap", C.c_float)]
+    _fields_ = [("kind", C.c_int32), ("epsilon", C.c_float), ("repulsion_cap", C.c_float),
+                ("has_repulsion_cap", C.c_int32)]
 
 
 class _TrainConfig(C.Structure):
@@ -210,8 +211,10 @@ class ForceModel:
 
     def _c(self) -> _ForceModel:
         kind = ForceKind.parse(self.kind) if isinstance(self.kind, str) else ForceKind(self.kind)
-        cap = -1.0 if self.repulsion_cap is None else float(self.repulsion_cap)
-        return _ForceModel(int(kind), float(self.epsilon), cap)
+        # std::optional<float>: None = no clamp; any float (0 included) clamps
+        has = self.repulsion_cap is not None
+        return _ForceModel(int(kind), float(self.epsilon),
+                           float(self.repulsion_cap) if has else 0.0, int(has))
 
 
 SAMPLERS = {"splitmix": 0, "reference": 0, "philox": 1}

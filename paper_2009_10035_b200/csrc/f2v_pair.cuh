@@ -152,7 +152,7 @@ struct Lay {
 //                          out   = (coef, 0, ..., 0)       (coincident fallback)
 // followed by  out_j *= scale  when clamped (force_kernels.cpp:69-77).
 struct Term {
-  double coef, inv, scale;
+  double coef, inv, scale, r;  // r = the distance (distance kinds)
   bool dist, fallback, clamped;
   double loss;
 };
@@ -212,6 +212,7 @@ __device__ __forceinline__ Term pair_term(int kind, const ForceParams& fp, bool 
     }
   }
   t.coef = scalar;
+  t.r = r_raw;
   t.fallback = r_raw < fp.eps;  // scaled_unit_diff, force_kernels.cpp:54-65
   t.inv = __ddiv_rn(1.0, r_raw);
   if (clamp_it && fp.has_cap) {
@@ -220,6 +221,17 @@ __device__ __forceinline__ Term pair_term(int kind, const ForceParams& fp, bool 
     if (t.clamped) t.scale = __ddiv_rn(fp.cap, m);
   }
   return t;
+}
+
+// The fp64 quotient x / t correctly rounded from inv = RN(1 / t): q = RN(x inv),
+// the exact residual x - q t (one fma), one correction fma (Markstein's
+// theorem: the result is RN(x / t) barring over/underflow).  Three fp64 ops
+// instead of a ~20-instruction division per column; checked against __ddiv_rn
+// (tests/test_gpu_parity.py::test_exact_quotient).
+__device__ __forceinline__ double div_by(double x, double t, double inv) {
+  const double q = __dmul_rn(x, inv);
+  const double r = __fma_rn(-q, t, x);
+  return __fma_rn(r, inv, q);
 }
 
 // acc += out(term) with the reference's rounding sequence.  w = the other
@@ -251,7 +263,7 @@ __device__ __forceinline__ void accumulate(const Term& t, int lane, const double
   }
 #pragma unroll
   for (int k = 0; k < K; ++k) {
-    double o = __dmul_rn(__dmul_rn(t.coef, w[k]), t.inv);
+    double o = div_by(__dmul_rn(t.coef, w[k]), t.r, t.inv);  // (c w) / t
     if (t.clamped) o = __dmul_rn(o, t.scale);
     acc[k] = __dadd_rn(acc[k], o);
   }
@@ -566,15 +578,23 @@ template <int KIND, int K, bool MON, bool ATT>
 __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t packed, int cnt,
                                             int lane, uint32_t d, const float* __restrict__ zold,
                                             const float* __restrict__ znew, const float (&zu)[K],
-                                            double (&acc)[K], double& lsum) {
+                                            double (&acc_io)[K], double& lsum_io) {
+  static_assert(KIND >= 0, "the EXACT vector path is compiled per force kind");
   using L = Lay<K, true>;
-  const int kind = KIND >= 0 ? KIND : fp.kind;
-  const bool sig = kind == F2V_SIGMOID;
+  constexpr bool SIG = KIND == F2V_SIGMOID;
+  // what a pair's term needs beyond its coefficient
+  constexpr bool SCALED = !ATT;       // repulsive kinds may be clamped (a second multiply)
   const int pi = pair_of_lane(lane);
   d = 32 * K;  // VEC layout: a compile-time row stride
-  double uu[K];
+  // the caller's accumulators live in its stack frame (Rows::run is out of
+  // line): work on register copies, written back once
+  double uu[K], acc[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k) uu[k] = zu[k];
+  for (int k = 0; k < K; ++k) {
+    uu[k] = zu[k];
+    acc[k] = acc_io[k];
+  }
+  double lsum = lsum_io;
   for (int k0 = 0; k0 < cnt; k0 += 8) {
     float v[8][K];
     uint32_t pks[8];
@@ -590,10 +610,22 @@ __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t pack
         for (int k = 0; k < K; ++k) v[i][k] = 0.0f;
       }
     }
+    {  // Znew rows not yet final: one vote for the block, then poll row by row
+      bool pend = false;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)  // Znew rows not yet final: poll
-      if (k0 + i < cnt && (pks[i] & kNewBit))
-        L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, v[i]);
+      for (int i = 0; i < 8; ++i)
+        if (k0 + i < cnt && (pks[i] & kNewBit))
+          pend |= has_sentinel<K, (K % 4 == 0) ? 2 : 1>(v[i]);
+      if (__any_sync(kFull, pend)) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (k0 + i < cnt && (pks[i] & kNewBit))
+            L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, v[i]);
+      }
+    }
+    // per-lane fp64 partial dot / distance of the 8 pairs.  Sigmoid: the
+    // products of two floats are exact in fp64, so fma(u, o, s) rounds exactly
+    // like the reference's separate multiply and add (force_kernels.cpp:30-34).
     double part[8], nrm[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -601,10 +633,10 @@ __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t pack
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const double o = double(v[i][k]);
-        if (sig) {
-          s = __dadd_rn(s, __dmul_rn(uu[k], o));
-          if (!ATT) q = __dadd_rn(q, __dmul_rn(o, o));
-        } else {
+        if (SIG) {
+          s = __fma_rn(uu[k], o, s);
+          if (!ATT) q = __fma_rn(o, o, q);
+        } else {  // distance(): diff * diff may be inexact -> separate roundings
           const double w = __dsub_rn(uu[k], o);
           s = __dadd_rn(s, __dmul_rn(w, w));
         }
@@ -613,32 +645,55 @@ __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t pack
       nrm[i] = q;
     }
     const double red = reduce8d(part, lane);
-    const double nr = (sig && !ATT) ? reduce8d(nrm, lane) : 0.0;
-    const Term t = pair_term<MON>(kind, fp, ATT, red, nr);  // pair pi, once per 4-lane group
+    const double nr = (SIG && !ATT) ? reduce8d(nrm, lane) : 0.0;
+    const Term t = pair_term<MON>(KIND, fp, ATT, red, nr);  // pair pi, once per 4-lane group
     if (MON && (lane & 3) == 0 && k0 + pi < cnt) lsum = __dadd_rn(lsum, t.loss);
-    const int tflags = (t.fallback ? 1 : 0) | (t.clamped ? 2 : 0);
+    // what each lane broadcasts: the coefficient, the clamp scale (1.0 when
+    // not clamped, applied only when clamped), the distance and 1/distance
+    const double sc = t.clamped ? t.scale : 1.0;
+    const int fl = (t.fallback ? 1 : 0) | (t.clamped ? 2 : 0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int src = lane_of_pair(i);
-      Term ti;
-      ti.dist = !sig;
-      const int f = __shfl_sync(kFull, tflags, src);
-      ti.fallback = f & 1;
-      ti.clamped = (f & 2) != 0;
-      ti.coef = __shfl_sync(kFull, t.coef, src);
-      ti.inv = sig ? 1.0 : __shfl_sync(kFull, t.inv, src);
-      ti.scale = ti.clamped ? __shfl_sync(kFull, t.scale, src) : 1.0;
-      if (k0 + i < cnt) {
-        double w[K];
+      const double c = __shfl_sync(kFull, t.coef, src);
+      const int f = (SCALED || !SIG) ? __shfl_sync(kFull, fl, src) : 0;
+      const double si = SCALED ? __shfl_sync(kFull, sc, src) : 1.0;
+      if (k0 + i >= cnt) continue;
+      if (SIG) {  // out_j = c z_j (x scale): scale_into + clamp_magnitude
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          const double o = double(v[i][k]);
-          w[k] = sig ? o : __dsub_rn(uu[k], o);
+          double o = __dmul_rn(c, double(v[i][k]));
+          if (SCALED && (f & 2)) o = __dmul_rn(o, si);
+          acc[k] = __dadd_rn(acc[k], o);
         }
-        accumulate<K>(ti, lane, w, acc);
+      } else {
+        const double tr = __shfl_sync(kFull, t.r, src);
+        const double inv = __shfl_sync(kFull, t.inv, src);
+        if (f & 1) {  // coincident: out = (c, 0, ..., 0) (scaled_unit_diff)
+          if (lane == 0) {
+            double o = c;
+            if (f & 2) o = __dmul_rn(o, si);
+            acc[0] = __dadd_rn(acc[0], o);
+          }
+          const double zero = (f & 2) ? __dmul_rn(0.0, si) : 0.0;
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            if (lane != 0 || k != 0) acc[k] = __dadd_rn(acc[k], zero);
+        } else {  // out_j = (c (u_j - o_j)) / t (force_kernels.cpp:63-64)
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const double w = __dsub_rn(uu[k], double(v[i][k]));
+            double o = div_by(__dmul_rn(c, w), tr, inv);
+            if (SCALED && (f & 2)) o = __dmul_rn(o, si);
+            acc[k] = __dadd_rn(acc[k], o);
+          }
+        }
       }
     }
   }
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc_io[k] = acc[k];
+  lsum_io = lsum;
 }
 
 // ------------------------------------------------------- FAST low-d
@@ -724,7 +779,7 @@ struct Rows {
       rows_lowd<KIND, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else if constexpr (FAST)
       rows_fast<KIND, K, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
-    else if constexpr (VEC)
+    else if constexpr (VEC && KIND >= 0)
       rows_exact8<KIND, K, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else
       rows_exact<KIND, K, VEC, 4, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc,

@@ -134,7 +134,7 @@ __global__ void sum_kernel(const double* __restrict__ v, uint64_t m, double* out
 ForceParams make_params(const f2v_force_model& m) {
   ForceParams p;
   p.kind = m.kind;
-  p.has_cap = m.repulsion_cap > 0 ? 1 : 0;
+  p.has_cap = m.has_repulsion_cap ? 1 : 0;  // std::optional<float> (force_kernels.cpp:72)
   p.eps = double(m.epsilon);
   p.cap = double(m.repulsion_cap);
   return p;

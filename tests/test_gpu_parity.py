@@ -113,6 +113,25 @@ def test_pair_golden_vectors_on_device(f2v, dev):
 
 
 # ---------------------------------------------------------- grad_minibatch
+def test_zero_repulsion_cap_on_device(f2v, orc, dev):
+    """repulsion_cap = 0.0 clamps (zero repulsion), None does not: the
+    explicit has_repulsion_cap flag of the C-ABI."""
+    rp, col = orc.orc_sbm_graph(300, 3, 0.05, 0.01, 2)
+    g = f2v.CsrGraph(rp, col)
+    z = np.zeros((300, 128), np.float32)
+    orc.oracle().orc_random_embedding(300, 128, 3, z)
+    dev.upload_graph(g)
+    dev.set_embedding(z)
+    ids = np.arange(0, 300, 7, dtype=np.uint32)
+    negs = np.array([5, 17, 99, 250, 3], np.uint32)
+    for kind in KINDS:
+        for cap in (0.0, None, 0.25):
+            got = dev.grad_minibatch(ids, negs, kind_model(f2v, kind, cap))
+            rc, ref, _ = orc.orc_grad_minibatch(rp, col, z, ids, negs, kind, cap=cap)
+            assert rc == 0
+            assert_grad_close(got, ref)
+
+
 @pytest.mark.parametrize("case", ["rg30", "rg80", "sbm256", "sbm300d2"])
 def test_grad_minibatch_vs_reference(f2v, dev, case):
     g = golden("grad.npz")

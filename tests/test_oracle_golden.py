@@ -154,7 +154,9 @@ def test_pair_grad_and_loss_bit_exact(orc):
     for i, (kind, att, d, rc, eps, cap) in enumerate(g["meta"]):
         d = int(d)
         zu, zo = g["zu"][i, :d], g["zo"][i, :d]
-        out = orc.orc_pair_grad(int(kind), zu, zo, int(att), eps=float(eps), cap=float(cap))
+        # the fixture encodes an unset repulsion_cap as -1
+        out = orc.orc_pair_grad(int(kind), zu, zo, int(att), eps=float(eps),
+                                cap=None if cap < 0 else float(cap))
         np.testing.assert_array_equal(out, g["grad"][i, :d])
         assert np.array_equal(out.astype(np.float32), g["grad_f32"][i, :d]) or \
             np.allclose(out, g["grad_f32"][i, :d], rtol=1e-6, atol=0)
@@ -175,7 +177,7 @@ def test_pair_grad_closed_forms(orc):
     a, b = np.array([1, 0], np.float32), np.array([0, 0], np.float32)
     assert np.all(orc.orc_pair_grad("tdist", a, a, 1) == 0)
     np.testing.assert_allclose(orc.orc_pair_grad("tdist", a, b, 1), [1, 0])
-    np.testing.assert_allclose(orc.orc_pair_grad("tdist", a, b, 0, cap=-1), [-1, 0])
+    np.testing.assert_allclose(orc.orc_pair_grad("tdist", a, b, 0, cap=None), [-1, 0])
     assert np.linalg.norm(orc.orc_pair_grad("tdist", a, a, 0)) == pytest.approx(5.0, rel=1e-5)
     u, o = np.array([3, 4], np.float32), np.zeros(2, np.float32)
     np.testing.assert_allclose(orc.orc_pair_grad("fr", u, o, 1), [15, 20])
@@ -284,3 +286,25 @@ def test_walk_mode_train_bit_exact(orc, k, kind):
     # work counters (acceptance.cpp:263-266): every non-isolated vertex walks k steps
     nonisolated = int((np.diff(ref["rowptr"]) > 0).sum())
     assert int(ctr[0]) == 2 * k * nonisolated and int(ctr[1]) == 2 * 300 * 5
+
+
+def test_zero_repulsion_cap_still_clamps(orc):
+    """std::optional<float>(0) is a cap (force_kernels.cpp:72-76): the
+    repulsive term scales to zero; only an unset cap skips the clamp
+    (ADVICE r1).  Checked against the compiled reference when present."""
+    rng = np.random.default_rng(5)
+    zu = rng.uniform(-1, 1, 16).astype(np.float32)
+    zo = rng.uniform(-1, 1, 16).astype(np.float32)
+    for kind in ("sigmoid", "tdist", "fr", "fa", "linlog"):
+        got = orc.orc_pair_grad(kind, zu, zo, 0, cap=0.0)
+        assert np.all(got == 0.0), (kind, got)
+        free = orc.orc_pair_grad(kind, zu, zo, 0, cap=None)
+        assert np.any(free != 0.0)
+        if orc.reference_available():
+            out = np.zeros(16, np.float64)
+            assert orc.reference().ref_pair_grad(orc.KINDS[kind], 1e-6, 0.0, zu, zo, 16, 0,
+                                                 out) == 0
+            assert np.array_equal(out, got)
+            assert orc.reference().ref_pair_grad(orc.KINDS[kind], 1e-6, float("nan"), zu, zo,
+                                                 16, 0, out) == 0
+            assert np.array_equal(out, free)
