@@ -79,7 +79,8 @@ typedef struct {
   int32_t precision;     /* F2V_PRECISION_FAST (default) or F2V_PRECISION_EXACT */
   uint32_t shards;       /* vertex shards G (0/1: the reference's single stream).  G > 1 =
                             the multi-GPU semantics: shard g owns
-                            rows [n g/G, n (g+1)/G), shuffles them with (seed,{0x22,epoch,g}),
+                            a contiguous row range cut at quantiles of deg(u) + s
+                            (f2v_shard_layout), shuffles it with (seed,{0x22,epoch,g}),
                             and step t = every shard's t-th batch on one snapshot.  On a
                             context attached to peers (f2v_shard_attach) G = the world
                             size and each GPU runs its own shard; otherwise one GPU runs
@@ -88,6 +89,12 @@ typedef struct {
                             k > 0 = walk mode: the context of u is a k-step random walk
                             (gen_walk, sampling.cpp:27-41) drawn on the batch stream before
                             the negatives; attractive_evals = k per non-isolated vertex */
+  uint32_t first_batch;  /* batch range of ONE epoch (run_epochs == 1, one-hop, one process):
+                            run only steps [first_batch, first_batch + run_batches) of epoch
+                            first_epoch, starting from the context's current Z as the state
+                            after step first_batch - 1 (per-step parity checks at any point
+                            of an epoch); run_batches 0 = the whole epoch (the default) */
+  uint32_t run_batches;
 } f2v_train_config;
 
 /* TrainCounters, trainer.hpp:83-87 */
@@ -216,10 +223,14 @@ void f2v_free(void* p);
  *                                       rows and stores every updated row into
  *                                       all replicas over NVLink.
  * Host-only helpers (no GPU needed): */
-/* combined step-major layout: poff_out[t*G + g] = first position of shard g's
- * batch t, poff_out[T*G] = n (poff_out nullable: *steps_out = T only) */
-int32_t f2v_shard_layout(uint32_t n, uint32_t batch, uint32_t shards, uint32_t* poff_out,
-                         uint32_t* steps_out);
+/* The G-shard layout of a graph: shard g owns rows
+ * [lo_out[g], lo_out[g+1]) (cut at quantiles of deg(u) + negatives), its local
+ * batch is batch_out[g]; combined step-major order: poff_out[t*G + g] = first
+ * position of shard g's batch t, poff_out[T*G] = n.  Every output is nullable
+ * (*steps_out = T alone sizes poff_out). */
+int32_t f2v_shard_layout(uint32_t n, const uint64_t* row_offsets, uint32_t negatives,
+                         uint32_t batch, uint32_t shards, uint32_t* lo_out, uint32_t* batch_out,
+                         uint32_t* poff_out, uint32_t* steps_out);
 /* partition_epoch (sampling.cpp:7-19) of one shard's n rows, keyed
  * (seed,{0x22,epoch}) when shards == 1 else (seed,{0x22,epoch,shard}) */
 int32_t f2v_partition_shard(uint32_t n, uint32_t b, uint64_t seed, uint32_t epoch,

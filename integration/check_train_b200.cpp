@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -35,8 +36,10 @@ int main(int argc, char** argv) {
   cfg.negatives = 5;
   cfg.epochs = 3;
   cfg.seed = 11;
-  cfg.monitor_loss = true;
   cfg.model.kind = argc > 2 ? parse_force_kind(argv[2]) : ForceKind::Sigmoid;
+  // pair_loss exists for sigmoid / tdist only (force_kernels.cpp:211-231)
+  const bool lossy = cfg.model.kind == ForceKind::Sigmoid || cfg.model.kind == ForceKind::TDist;
+  cfg.monitor_loss = lossy;
   TrainResult mine;
   try {
     mine = train_b200(g, cfg, {}, 0);
@@ -57,8 +60,25 @@ int main(int argc, char** argv) {
     same += a[i] == b[i];
   }
   std::printf("OK %.3e %.6f %.17g %.17g %llu %llu\n", worst, double(same) / double(a.size()),
-              mine.epoch_loss.back(), ref.epoch_loss.back(),
+              lossy ? mine.epoch_loss.back() : 0.0, lossy ? ref.epoch_loss.back() : 0.0,
               (unsigned long long)mine.counters.attractive_evals,
               (unsigned long long)ref.counters.attractive_evals);
+  if (!lossy) {  // monitoring: UnsupportedError with the same message on both sides
+    cfg.monitor_loss = true;
+    std::string m1 = "-", m2 = "-";
+    try {
+      train_b200(g, cfg, {}, 0);
+    } catch (const UnsupportedError& ex) {
+      m1 = ex.what();
+    } catch (const std::exception&) {
+    }
+    try {
+      train(g, cfg);
+    } catch (const UnsupportedError& ex) {
+      m2 = ex.what();
+    } catch (const std::exception&) {
+    }
+    std::printf("UNSUPPORTED %d %d\n", m1 != "-", int(m1 == m2));
+  }
   return 0;
 }

@@ -385,9 +385,49 @@ int orc_batch_loss(const uint64_t* rowptr, const uint32_t* col, const float* z,
 }
 
 /* ------------------------------------------------------ trainer.cpp:192-251 */
-void orc_shard_range(uint32_t n, uint32_t G, uint32_t g, uint32_t* lo, uint32_t* hi) {
-  *lo = (uint32_t)((uint64_t)n * g / G);
-  *hi = (uint32_t)((uint64_t)n * (g + 1) / G);
+/* Vertex shards of a G-GPU run (no reference
+ * counterpart -- the reference is single-process).  G == 1 is exactly
+ * train(): one shard, batch min(batch, n) (trainer.cpp:200).  G > 1:
+ *   - contiguous row ranges cut at quantiles of the per-vertex work
+ *     w(u) = deg(u) + s (its pair evaluations per epoch): lo[g] is the first u
+ *     whose work prefix reaches floor(g W / G), W = nnz + n s, kept strictly
+ *     increasing so every shard owns at least one row;
+ *   - T = ceil(n / (G batch)) steps; shard g's local batch is
+ *     ceil(size_g / T), so every shard finishes in (at most) T steps and the
+ *     per-step work is balanced as well as the per-epoch work. */
+void orc_shard_layout(const uint64_t* rowptr, uint32_t n, uint32_t G, uint32_t s,
+                      uint32_t batch, uint32_t* lo, uint32_t* bs, uint32_t* nb, uint64_t* T) {
+  lo[0] = 0;
+  lo[G] = n;
+  if (G == 1) {
+    bs[0] = batch < n ? batch : n;
+    nb[0] = (n + bs[0] - 1) / bs[0];
+    *T = nb[0];
+    return;
+  }
+  const uint64_t W = rowptr[n] + (uint64_t)n * s;
+  for (uint32_t g = 1; g < G; ++g) {
+    const uint64_t target = W * g / G;
+    uint32_t a = 0, b = n; /* first u in [0, n] with rowptr[u] + u s >= target */
+    while (a < b) {
+      const uint32_t m = a + (b - a) / 2;
+      if (rowptr[m] + (uint64_t)m * s >= target) b = m; else a = m + 1;
+    }
+    uint32_t x = a;
+    if (x < lo[g - 1] + 1) x = lo[g - 1] + 1;
+    if (x > n - (G - g)) x = n - (G - g);
+    lo[g] = x;
+  }
+  const uint64_t gb = (uint64_t)G * batch;
+  const uint64_t steps = ((uint64_t)n + gb - 1) / gb;
+  uint64_t t = 0;
+  for (uint32_t g = 0; g < G; ++g) {
+    const uint32_t sz = lo[g + 1] - lo[g];
+    bs[g] = (uint32_t)(((uint64_t)sz + steps - 1) / steps);
+    nb[g] = (sz + bs[g] - 1) / bs[g];
+    if (nb[g] > t) t = nb[g];
+  }
+  *T = t;
 }
 
 /* gen_walk (sampling.cpp:27-41): k steps from u on the stream st (one below()
@@ -437,21 +477,15 @@ int orc_train_mode(const uint64_t* rowptr, const uint32_t* col, uint32_t n, floa
   const uint32_t* xcol = walk_k ? ccol : col;
   if (monitor && kind != ORC_SIGMOID && kind != ORC_TDIST) return 6;
   uint32_t* perms = (uint32_t*)malloc(sizeof(uint32_t) * n);
-  uint32_t* lo = (uint32_t*)malloc(sizeof(uint32_t) * G);
+  uint32_t* lo = (uint32_t*)malloc(sizeof(uint32_t) * (G + 1));
   uint32_t* bs = (uint32_t*)malloc(sizeof(uint32_t) * G);
   uint32_t* nb = (uint32_t*)malloc(sizeof(uint32_t) * G);
   uint32_t* negs = (uint32_t*)malloc(sizeof(uint32_t) * s * G);
   uint32_t bmax = 0;
   uint64_t T = 0;
-  for (uint32_t g = 0; g < G; ++g) {
-    uint32_t l, h;
-    orc_shard_range(n, G, g, &l, &h);
-    lo[g] = l;
-    bs[g] = batch < (h - l) ? batch : (h - l); /* trainer.cpp:200 */
-    nb[g] = (h - l + bs[g] - 1) / bs[g];
+  orc_shard_layout(rowptr, n, G, s, batch, lo, bs, nb, &T);
+  for (uint32_t g = 0; g < G; ++g)
     if (bs[g] > bmax) bmax = bs[g];
-    if (nb[g] > T) T = nb[g];
-  }
   float* grads = (float*)malloc(sizeof(float) * (size_t)bmax * d * G);
   uint64_t attr = 0, rep = 0;
   int rc = 0;
@@ -459,8 +493,7 @@ int orc_train_mode(const uint64_t* rowptr, const uint32_t* col, uint32_t n, floa
     float eta = lr;
     if (lr_decay) eta = lr * (1.0f - (float)epoch / (float)epochs); /* 212-214 */
     for (uint32_t g = 0; g < G; ++g) {
-      uint32_t l, h;
-      orc_shard_range(n, G, g, &l, &h);
+      const uint32_t l = lo[g], h = lo[g + 1];
       const uint64_t key1[2] = {0x22, epoch}, keyG[3] = {0x22, epoch, g};
       const uint64_t st = G == 1 ? orc_rng_keyed(seed, key1, 2) : orc_rng_keyed(seed, keyG, 3);
       orc_partition(h - l, bs[g], st, perms + l);
@@ -475,8 +508,7 @@ int orc_train_mode(const uint64_t* rowptr, const uint32_t* col, uint32_t n, floa
         const uint64_t key3[3] = {0x33, epoch, t}, key4[4] = {0x33, epoch, t, g};
         uint64_t st = G == 1 ? orc_rng_keyed(seed, key3, 3) : orc_rng_keyed(seed, key4, 4);
         if (walk_k && t < nb[g]) {
-          uint32_t l, h;
-          orc_shard_range(n, G, g, &l, &h);
+          const uint32_t l = lo[g], h = lo[g + 1];
           const uint32_t p0 = l + (uint32_t)(t * bs[g]);
           const uint32_t p1 = (uint32_t)((uint64_t)p0 + bs[g] < h ? p0 + bs[g] : h);
           for (uint32_t p = p0; p < p1; ++p)
@@ -491,8 +523,7 @@ int orc_train_mode(const uint64_t* rowptr, const uint32_t* col, uint32_t n, floa
       /* gradients of every shard's batch on the same snapshot */
       for (uint32_t g = 0; g < G && rc == 0; ++g) {
         if (t >= nb[g]) continue;
-        uint32_t l, h;
-        orc_shard_range(n, G, g, &l, &h);
+        const uint32_t l = lo[g], h = lo[g + 1];
         const uint32_t p0 = l + (uint32_t)(t * bs[g]);
         const uint32_t p1 = (uint32_t)((uint64_t)p0 + bs[g] < h ? p0 + bs[g] : h);
         uint32_t bad = 0;
@@ -516,8 +547,7 @@ int orc_train_mode(const uint64_t* rowptr, const uint32_t* col, uint32_t n, floa
       if (rc) break;
       for (uint32_t g = 0; g < G; ++g) {
         if (t >= nb[g]) continue;
-        uint32_t l, h;
-        orc_shard_range(n, G, g, &l, &h);
+        const uint32_t l = lo[g], h = lo[g + 1];
         const uint32_t p0 = l + (uint32_t)(t * bs[g]);
         const uint32_t p1 = (uint32_t)((uint64_t)p0 + bs[g] < h ? p0 + bs[g] : h);
         orc_apply_update(z, d, perms + p0, p1 - p0, grads + (size_t)g * bmax * d, eta);

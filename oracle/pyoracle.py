@@ -91,8 +91,8 @@ def oracle():
                                           C.c_float, C.c_float, C.c_uint64, C.c_int, C.c_int,
                                           C.c_int, C.c_uint32, C.c_uint32, C.c_int, f64p, u64p,
                                           STEP_CB, C.c_void_p, u32p])
-        _sig(L, "orc_shard_range", None, [C.c_uint32, C.c_uint32, C.c_uint32,
-                                        C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)])
+        _sig(L, "orc_shard_layout", None, [u64p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                         C.c_uint32, u32p, u32p, u32p, C.POINTER(C.c_uint64)])
         _orc = L
     return _orc
 
@@ -275,6 +275,18 @@ def ref_graph_from_edges(pairs, n, symmetrize=True):
                                                      C.byref(loops)))
 
 
+def orc_shard_layout(rowptr, G, s, batch):
+    """(lo[G+1], bs[G], nb[G], T) of the G-shard run (oracle/f2v_oracle.c)."""
+    rowptr = np.ascontiguousarray(rowptr, np.uint64)
+    n = len(rowptr) - 1
+    lo = np.zeros(G + 1, np.uint32)
+    bs = np.zeros(G, np.uint32)
+    nb = np.zeros(G, np.uint32)
+    T = C.c_uint64()
+    oracle().orc_shard_layout(rowptr, n, G, s, batch, lo, bs, nb, C.byref(T))
+    return lo, bs, nb, T.value
+
+
 def orc_rng_keyed(seed, key):
     k = np.ascontiguousarray(key if len(key) else [0], np.uint64)
     return oracle().orc_rng_keyed(seed, k, len(key))
@@ -370,4 +382,42 @@ def orc_train(rowptr, col, z0, batch, s, lr, epochs, kind, seed, eps=1e-6, cap=5
                                  s, lr, epochs, KINDS.get(kind, kind), eps, capv(cap), seed,
                                  int(lr_decay), int(monitor), 1 if sampler in ("philox", 1) else 0,
                                  G, walk, threads, losses, counters, cb, None, fail)
+    return rc, z, losses, counters, fail
+
+
+def ref_train(rg, z0, batch, s, lr, epochs, kind, seed, eps=1e-6, cap=5.0, lr_decay=False,
+              monitor=True, sampler="philox", workers=None, step_cb=None, walk=0):
+    """The UNMODIFIED reference train() loop (trainer.cpp:192-251, oracle/_ref)
+    on a RefGraph with an injected initial Z; sampler "philox" injects the
+    configs' Philox negatives into each Minibatch (the reference's own
+    partition_epoch perm is kept).  step_cb(epoch, batch, z_view) runs after
+    every apply_update.  Returns (rc, Z, epoch_losses, counters, fail_info)."""
+    import ctypes as C
+    R = reference()
+    z = np.array(z0, np.float32, copy=True, order="C")
+    n, d = z.shape
+    b = min(batch, n)
+    nb = (n + b - 1) // b
+    negs = None
+    if sampler in ("philox", 1):
+        negs = np.zeros(epochs * nb * s, np.uint32)
+        for e in range(epochs):
+            for bi in range(nb):
+                o = (e * nb + bi) * s
+                negs[o:o + s] = orc_negatives("philox", seed, e, bi, n, s)
+    losses = np.zeros(epochs, np.float64)
+    counters = np.zeros(2, np.uint64)
+    fail = np.zeros(3, np.uint32)
+    if step_cb is not None:
+        def _cb(e, t, zp, user):
+            step_cb(e, t, np.ctypeslib.as_array(zp, shape=(n, d)))
+        cb = STEP_CB(_cb)
+    else:
+        cb = STEP_CB()
+    rc = R.ref_train_mode(rg.ptr, z, d, batch, s, lr, epochs, KINDS.get(kind, kind), eps,
+                          capv(cap), seed, workers or os.cpu_count() or 4, int(lr_decay),
+                          int(monitor), walk, None,
+                          negs.ctypes.data_as(C.c_void_p) if negs is not None else None,
+                          losses, counters, C.cast(cb, C.c_void_p) if step_cb else None, None,
+                          fail)
     return rc, z, losses, counters, fail

@@ -85,7 +85,8 @@ class _TrainConfig(C.Structure):
                 ("seed", C.c_uint64), ("lr_decay", C.c_int32), ("monitor_loss", C.c_int32),
                 ("sampler", C.c_int32), ("init", C.c_int32), ("first_epoch", C.c_uint32),
                 ("run_epochs", C.c_uint32), ("precision", C.c_int32), ("shards", C.c_uint32),
-                ("walk_length", C.c_uint32)]
+                ("walk_length", C.c_uint32), ("first_batch", C.c_uint32),
+                ("run_batches", C.c_uint32)]
 
 
 class _Counters(C.Structure):
@@ -148,7 +149,8 @@ SYMBOLS = {
     "f2v_gen_rgg": (_i32, [C.c_uint32, C.c_double, C.c_uint64, C.POINTER(C.POINTER(C.c_uint32)),
                            C.POINTER(C.c_uint64)]),
     "f2v_free": (None, [_vp]),
-    "f2v_shard_layout": (_i32, [C.c_uint32, C.c_uint32, C.c_uint32, _vp, C.POINTER(C.c_uint32)]),
+    "f2v_shard_layout": (_i32, [C.c_uint32, _u64p, C.c_uint32, C.c_uint32, C.c_uint32, _vp, _vp,
+                                _vp, C.POINTER(C.c_uint32)]),
     "f2v_shard_handle_bytes": (_i32, []),
     "f2v_shard_init": (_i32, [_vp, C.c_uint32, C.c_uint32]),
     "f2v_shard_export": (_i32, [_vp, C.c_char_p]),
@@ -238,7 +240,8 @@ class TrainConfig:
     shards: int = 1  # vertex shards G; 1 = the reference's stream
     walk_length: int = 0  # SampleMode: 0 one-hop, k > 0 walk mode (sampling.hpp:12-20)
 
-    def _c(self, init: int = 0, first_epoch: int = 0, run_epochs: int = 0) -> _TrainConfig:
+    def _c(self, init: int = 0, first_epoch: int = 0, run_epochs: int = 0, first_batch: int = 0,
+           run_batches: int = 0) -> _TrainConfig:
         if self.lr_decay not in ("constant", "linear_to_zero"):
             raise UsageError("lr_decay must be constant or linear_to_zero")
         if self.sampler not in SAMPLERS:
@@ -252,7 +255,7 @@ class TrainConfig:
                             int(self.lr_decay == "linear_to_zero"), int(self.monitor_loss),
                             SAMPLERS[self.sampler], init, first_epoch, run_epochs,
                             0 if self.precision == "fast" else 1, int(self.shards),
-                            int(self.walk_length))
+                            int(self.walk_length), int(first_batch), int(run_batches))
 
 
 @dataclasses.dataclass
@@ -358,19 +361,21 @@ def partition_epoch(n: int, b: int, seed: int, epoch: int) -> np.ndarray:
     return perm
 
 
-def shard_layout(n: int, batch: int, shards: int):
-    """(poff, T): combined step-major layout of G shards (f2v_shard_layout):
-    poff[t*G + g] = first position of shard g's batch t, poff[T*G] = n."""
+def shard_layout(g: "CsrGraph", batch: int, shards: int, negatives: int):
+    """The G-shard layout of graph g (f2v_shard_layout):
+    (lo[G+1], local batch[G], poff, T) -- shard i owns rows [lo[i], lo[i+1]),
+    poff[t*G + i] = first combined position of shard i's batch t, poff[T*G] = n."""
+    n = g.num_vertices()
     T = C.c_uint32()
-    _check(_lib.f2v_shard_layout(n, batch, shards, None, C.byref(T)))
+    _check(_lib.f2v_shard_layout(n, g.row_offsets, negatives, batch, shards, None, None, None,
+                                 C.byref(T)))
+    lo = np.zeros(shards + 1, np.uint32)
+    bs = np.zeros(shards, np.uint32)
     poff = np.zeros(T.value * shards + 1, np.uint32)
-    _check(_lib.f2v_shard_layout(n, batch, shards, poff.ctypes.data_as(_vp), C.byref(T)))
-    return poff, T.value
-
-
-def shard_range(n: int, shards: int, g: int):
-    """rows [lo, hi) of shard g (orc_shard_range)"""
-    return n * g // shards, n * (g + 1) // shards
+    _check(_lib.f2v_shard_layout(n, g.row_offsets, negatives, batch, shards,
+                                 lo.ctypes.data_as(_vp), bs.ctypes.data_as(_vp),
+                                 poff.ctypes.data_as(_vp), C.byref(T)))
+    return lo, bs, poff, T.value
 
 
 def partition_shard(n: int, b: int, seed: int, epoch: int, shard: int, shards: int) -> np.ndarray:
@@ -549,10 +554,15 @@ class Device:
 
     def train_epochs(self, cfg: TrainConfig, first_epoch: int = 0, run_epochs: int = 0,
                      init: bool = False, counters: Optional[TrainCounters] = None,
-                     failure: Optional[dict] = None) -> list:
+                     failure: Optional[dict] = None, first_batch: int = 0,
+                     run_batches: int = 0) -> list:
         """Device-resident epochs [first_epoch, first_epoch + run_epochs) of
-        train()'s cfg.epochs-long schedule (run_epochs 0: through the end)."""
-        c = cfg._c(init=1 if init else 0, first_epoch=first_epoch, run_epochs=run_epochs)
+        train()'s cfg.epochs-long schedule (run_epochs 0: through the end).
+        run_batches > 0 (with run_epochs == 1): only steps [first_batch,
+        first_batch + run_batches) of that epoch, from the current Z taken as
+        the state after step first_batch - 1 (per-step parity anywhere)."""
+        c = cfg._c(init=1 if init else 0, first_epoch=first_epoch, run_epochs=run_epochs,
+                   first_batch=first_batch, run_batches=run_batches)
         end = min(cfg.epochs, first_epoch + run_epochs) if run_epochs else cfg.epochs
         nep = max(end - first_epoch, 0)
         losses = np.zeros(max(nep, 1), np.float64)

@@ -164,7 +164,7 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
       cfg.run_epochs ? std::min(cfg.epochs, cfg.first_epoch + cfg.run_epochs) : cfg.epochs;
   validate_model(cfg.model);
   if (cfg.monitor_loss && cfg.model.kind != F2V_SIGMOID && cfg.model.kind != F2V_TDIST)
-    fail(F2V_EUNSUPPORTED, "loss monitoring requires the sigmoid or tdist model");
+    fail(F2V_EUNSUPPORTED, "loss monitoring requires the sigmoid or tdist model");  // trainer.cpp:195-197
   if (cfg.sampler != F2V_SAMPLER_SPLITMIX && cfg.sampler != F2V_SAMPLER_PHILOX)
     fail(F2V_EUSAGE, "unknown sampler");
   if (c.n >= 0x80000000u) fail(F2V_EUSAGE, "n must be < 2^31");
@@ -192,8 +192,24 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
     if (!cfg.shards) G = c.world;
     if (G != c.world) fail(F2V_EUSAGE, "cfg.shards must equal the number of attached GPUs");
   }
-  k_shard_layout(c, cfg.batch, G);  // batch clamped per shard (trainer.cpp:200)
+  k_shard_layout(c, cfg.batch, G, s);  // batch clamped per shard (trainer.cpp:200)
   k_set_context(c, cfg.walk_length);  // SampleMode: one-hop CSR or k-step walks
+  // a batch range of one epoch: steps [t0, t1) from the current Z
+  c.ranged = cfg.run_batches > 0;
+  if (c.ranged) {
+    if (end_epoch != cfg.first_epoch + 1) fail(F2V_EUSAGE, "a batch range needs run_epochs == 1");
+    if (cfg.walk_length) fail(F2V_EUSAGE, "batch ranges are one-hop only");
+    if (c.shard_ready) fail(F2V_EUSAGE, "batch ranges need a single-process context");
+    if (cfg.first_batch >= c.steps) fail(F2V_EUSAGE, "first_batch beyond the epoch's steps");
+    c.range_t0 = cfg.first_batch;
+    c.range_t1 = uint32_t(std::min<uint64_t>(c.steps, uint64_t(cfg.first_batch) + cfg.run_batches));
+    c.range_p0 = c.h_poff[size_t(c.range_t0) * G];
+    c.range_p1 = c.h_poff[size_t(c.range_t1) * G];
+  }
+  struct RangeReset {  // the context runs whole epochs again after this call
+    Ctx& c;
+    ~RangeReset() { c.ranged = false; }
+  } range_reset{c};
   uint64_t attr = 0, rep = 0;
   for (uint32_t e = cfg.first_epoch; e < end_epoch; ++e) {
     float eta = cfg.lr;
@@ -221,6 +237,17 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
                                std::to_string(e) + ", batch " + std::to_string(jb) + ")");
     }
     if (cfg.monitor_loss && loss_out) loss_out[e - cfg.first_epoch] = r.loss;
+    if (c.ranged) {
+      // rows outside the range keep their given values (state "after every step")
+      k_epoch_restore(c, c.range_t1);
+      std::vector<uint32_t> ids(c.range_p1 - c.range_p0);
+      if (!ids.empty())
+        F2V_CUDA(cudaMemcpy(ids.data(), c.perm.as<uint32_t>() + c.range_p0,
+                            sizeof(uint32_t) * ids.size(), cudaMemcpyDeviceToHost));
+      attr += degree_sum(c, ids.data(), uint32_t(ids.size()));
+      rep += uint64_t(ids.size()) * s;
+      continue;
+    }
     attr += c.nnz;            // one-hop: every arc once per epoch (trainer.cpp:154-160)
     rep += uint64_t(n) * s;   // b*s per batch (trainer.cpp:161-162)
   }
@@ -281,6 +308,7 @@ void f2v_destroy(f2v_ctx* h) {
     for (int i = 0; i < 3; ++i)
       if (c.peer_base[g][i]) cudaIpcCloseMemHandle(c.peer_base[g][i]);
   c.ctl.release();
+  for (DeviceBuf& r : c.rep) r.release();
   for (cudaEvent_t e : c.ev_kernel) cudaEventDestroy(e);
   if (c.ev_begin) cudaEventDestroy(c.ev_begin);
   if (c.ev_end) cudaEventDestroy(c.ev_end);
@@ -330,6 +358,7 @@ int32_t f2v_upload_graph(f2v_ctx* h, uint32_t n, const uint64_t* row_offsets,
     }
     c.n = n;
     c.nnz = nnz;
+    ++c.graph_gen;  // shard layouts depend on the degrees
     c.h_rowptr.assign(row_offsets, row_offsets + n + 1);
     c.rowptr.ensure(sizeof(uint64_t) * (n + 1));
     c.col.ensure(sizeof(uint32_t) * std::max<uint64_t>(nnz, 1));
@@ -457,7 +486,7 @@ int32_t f2v_batch_loss(f2v_ctx* h, const uint32_t* ids, uint32_t b, const uint32
     need_embedding(c);
     validate_model(model);
     if (model.kind != F2V_SIGMOID && model.kind != F2V_TDIST)
-      fail(F2V_EUNSUPPORTED, "batch_loss is defined for sigmoid and tdist only");
+      fail(F2V_EUNSUPPORTED, "pair_loss is defined for sigmoid and tdist only");
     F2V_CUDA(cudaSetDevice(c.device));
     stage_batch(c, ids, b, negs, s);
     k_grad_minibatch(c, b, s, make_params(model), true);
@@ -477,7 +506,7 @@ int32_t f2v_step(f2v_ctx* h, const uint32_t* ids, uint32_t b, const uint32_t* ne
     validate_model(model);
     const bool mon = loss_out != nullptr;
     if (mon && model.kind != F2V_SIGMOID && model.kind != F2V_TDIST)
-      fail(F2V_EUNSUPPORTED, "batch_loss is defined for sigmoid and tdist only");
+      fail(F2V_EUNSUPPORTED, "pair_loss is defined for sigmoid and tdist only");
     F2V_CUDA(cudaSetDevice(c.device));
     const bool uniq = stage_batch(c, ids, b, negs, s);
     k_grad_minibatch(c, b, s, make_params(model), mon);
@@ -618,13 +647,16 @@ int32_t f2v_gen_rgg(uint32_t n, double mean_deg, uint64_t seed, uint32_t** pairs
 void f2v_free(void* p) { std::free(p); }
 
 // ------------------------------------------ multi-GPU shards (f2v_shard.cu)
-int32_t f2v_shard_layout(uint32_t n, uint32_t batch, uint32_t shards, uint32_t* poff_out,
-                         uint32_t* steps_out) {
+int32_t f2v_shard_layout(uint32_t n, const uint64_t* row_offsets, uint32_t negatives,
+                         uint32_t batch, uint32_t shards, uint32_t* lo_out, uint32_t* batch_out,
+                         uint32_t* poff_out, uint32_t* steps_out) {
   return guard(nullptr, [&] {
     std::vector<uint32_t> lo, bs, nb, poff;
     uint32_t T = 0;
-    shard_layout(n, batch, shards, lo, bs, nb, poff, T);
+    shard_layout(row_offsets, n, negatives, batch, shards, lo, bs, nb, poff, T);
     if (steps_out) *steps_out = T;
+    if (lo_out) std::memcpy(lo_out, lo.data(), sizeof(uint32_t) * lo.size());
+    if (batch_out) std::memcpy(batch_out, bs.data(), sizeof(uint32_t) * bs.size());
     if (poff_out) std::memcpy(poff_out, poff.data(), sizeof(uint32_t) * poff.size());
   });
 }

@@ -49,8 +49,11 @@ using namespace dev;
 // Shard geometry for the device (G <= kMaxShards).
 struct ShardGeo {
   uint32_t n, G, rank_lo, rank_hi;  // owned rows [rank_lo, rank_hi) (all: [0, n))
+  uint32_t p_lo, p_hi;              // positions run this launch (a batch range; all: [0, n))
   uint32_t lo[ep::kMaxShards + 1], bs[ep::kMaxShards], nb[ep::kMaxShards];
 };
+
+constexpr uint32_t kOutsideRange = 0xfffffffeu;  // step 0x7fffffff: after every step
 
 // Combined step-major order: local position i of shard g (its Fisher-Yates
 // perm in lperm[lo_g + i]) lands at poff[t G + g] + i % bs_g with t = i / bs_g
@@ -66,14 +69,17 @@ __global__ void scatter_kernel(const uint32_t* __restrict__ lperm, const uint32_
     nE[geo.n] = 0;
     return;
   }
-  const uint32_t g = ep::shard_of(x, geo.n, geo.G);
+  const uint32_t g = ep::shard_of(x, geo.lo, geo.G);
   const uint32_t i = x - geo.lo[g];
   const uint32_t u = geo.lo[g] + lperm[x];
   const uint32_t t = i / geo.bs[g];
   const uint32_t pos = poff[t * geo.G + g] + i % geo.bs[g];
   perm[pos] = u;
-  state[u] = t << 1;
-  const bool own = u >= geo.rank_lo && u < geo.rank_hi;
+  const bool run = pos >= geo.p_lo && pos < geo.p_hi;
+  // a vertex outside a batch range is final in Z as given (before or after
+  // the range): its step reads as "later than every step" -> always Zold
+  state[u] = run ? t << 1 : kOutsideRange;
+  const bool own = run && u >= geo.rank_lo && u < geo.rank_hi;
   nE[pos] = own ? cbase[u + 1] - cbase[u] : 0u;
   wtot[u] = 0;
 }
@@ -142,8 +148,14 @@ __global__ void needs_kernel(const uint32_t* __restrict__ perm, ShardGeo geo,
     return;
   }
   const uint32_t u = perm[p];
+  if (p < geo.p_lo || p >= geo.p_hi) {  // outside a batch range: no work
+    needs[u] = 0;
+    nL[p] = 0;
+    pcnt[p] = 0;
+    return;
+  }
   const uint32_t j = state[u] >> 1;
-  const uint32_t nw = negwin[geo.G == 1 ? j : j * geo.G + ep::shard_of(u, n, geo.G)];
+  const uint32_t nw = negwin[geo.G == 1 ? j : j * geo.G + ep::shard_of(u, geo.lo, geo.G)];
   uint32_t nd = ((wtot[u] | nw) & 1u) && !nodep ? 1u : 0u;
   needs[u] = nd;
   const bool own = u >= geo.rank_lo && u < geo.rank_hi;
@@ -237,6 +249,16 @@ __global__ void restore_kernel(const uint32_t* __restrict__ state, const float* 
   if ((state[v] >> 1) >= jb) znew[t] = zold[t];
 }
 
+// replica emulation: count the words where replica r differs from the primary
+__global__ void replica_diff_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
+                                    uint64_t m, unsigned long long* diff) {
+  unsigned long long c = 0;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    c += a[i] != b[i];
+  if (c) atomicAdd(diff, c);
+}
+
 __global__ void zero_kernel(double* __restrict__ v, uint64_t m) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < m) v[i] = 0.0;
@@ -321,26 +343,48 @@ void k_prepare_graph(Ctx& c) {
   F2V_CUDA(cudaStreamSynchronize(c.stream));
 }
 
-// Host: shard g of G owns rows [n g / G, n (g+1) / G) (orc_shard_range) with
-// batch bs_g = min(batch, size_g) (trainer.cpp:200) and nb_g local batches.
-// Step t = the t-th local batch of every shard, laid out shard by shard:
-// poff[t G + g] = combined position of shard g's batch t; poff[T G] = n.
-void shard_layout(uint32_t n, uint32_t batch, uint32_t G, std::vector<uint32_t>& lo,
-                  std::vector<uint32_t>& bs, std::vector<uint32_t>& nb,
-                  std::vector<uint32_t>& poff, uint32_t& T) {
+// Host: the G-shard layout (orc_shard_layout).  G == 1
+// is train()'s single shard (batch min(batch, n), trainer.cpp:200).  G > 1:
+// contiguous row ranges cut at quantiles of the per-vertex work deg(u) + s
+// (R-MAT's hub rows no longer pile onto shard 0), T = ceil(n / (G batch))
+// steps and shard g's local batch ceil(size_g / T), so the per-step work is
+// balanced too.  Step t = the t-th local batch of every shard, laid out shard
+// by shard: poff[t G + g] = combined position of shard g's batch t; poff[T G] = n.
+void shard_layout(const uint64_t* rowptr, uint32_t n, uint32_t s, uint32_t batch, uint32_t G,
+                  std::vector<uint32_t>& lo, std::vector<uint32_t>& bs,
+                  std::vector<uint32_t>& nb, std::vector<uint32_t>& poff, uint32_t& T) {
   if (G < 1 || G > uint32_t(ep::kMaxShards)) fail(F2V_EUSAGE, "shards must be in [1, 8]");
   if (n < G) fail(F2V_EUSAGE, "fewer vertices than shards");
   if (batch < 1) fail(F2V_EUSAGE, "batch must be >= 1");
   lo.assign(G + 1, 0);
   bs.assign(G, 0);
   nb.assign(G, 0);
+  lo[G] = n;
   T = 0;
-  for (uint32_t g = 0; g <= G; ++g) lo[g] = uint32_t(uint64_t(n) * g / G);
-  for (uint32_t g = 0; g < G; ++g) {
-    const uint32_t sz = lo[g + 1] - lo[g];
-    bs[g] = std::min(batch, sz);
-    nb[g] = (sz + bs[g] - 1) / bs[g];
-    T = std::max(T, nb[g]);
+  if (G == 1) {
+    bs[0] = std::min(batch, n);
+    nb[0] = (n + bs[0] - 1) / bs[0];
+    T = nb[0];
+  } else {
+    const uint64_t W = rowptr[n] + uint64_t(n) * s;
+    for (uint32_t g = 1; g < G; ++g) {
+      const uint64_t target = W * g / G;
+      uint32_t a = 0, b = n;  // first u in [0, n] whose work prefix reaches the target
+      while (a < b) {
+        const uint32_t m = a + (b - a) / 2;
+        if (rowptr[m] + uint64_t(m) * s >= target) b = m;
+        else a = m + 1;
+      }
+      lo[g] = std::min(std::max(a, lo[g - 1] + 1), n - (G - g));
+    }
+    const uint64_t gb = uint64_t(G) * batch;
+    const uint64_t steps = (uint64_t(n) + gb - 1) / gb;
+    for (uint32_t g = 0; g < G; ++g) {
+      const uint32_t sz = lo[g + 1] - lo[g];
+      bs[g] = uint32_t((uint64_t(sz) + steps - 1) / steps);
+      nb[g] = (sz + bs[g] - 1) / bs[g];
+      T = std::max(T, nb[g]);
+    }
   }
   poff.assign(size_t(T) * G + 1, 0);
   uint64_t pos = 0;
@@ -352,18 +396,18 @@ void shard_layout(uint32_t n, uint32_t batch, uint32_t G, std::vector<uint32_t>&
   poff[size_t(T) * G] = uint32_t(pos);
 }
 
-void k_shard_layout(Ctx& c, uint32_t batch, uint32_t G) {
-  if (c.layout_key[0] == c.n && c.layout_key[1] == batch && c.layout_key[2] == G && c.steps)
-    return;
-  shard_layout(c.n, batch, G, c.sh_lo, c.sh_bs, c.sh_nb, c.h_poff, c.steps);
+void k_shard_layout(Ctx& c, uint32_t batch, uint32_t G, uint32_t s) {
+  const uint64_t key[4] = {c.graph_gen, batch, G, s};
+  if (c.steps && std::equal(key, key + 4, c.layout_key)) return;
+  // the graph's degrees, also while a walk context is active (f2v_walk.cu)
+  const std::vector<uint64_t>& rp = c.walk_k ? c.h_growptr : c.h_rowptr;
+  shard_layout(rp.data(), c.n, s, batch, G, c.sh_lo, c.sh_bs, c.sh_nb, c.h_poff, c.steps);
   c.poff.ensure(sizeof(uint32_t) * c.h_poff.size());
   F2V_CUDA(cudaMemcpyAsync(c.poff.p, c.h_poff.data(), sizeof(uint32_t) * c.h_poff.size(),
                            cudaMemcpyHostToDevice, c.stream));
   F2V_CUDA(cudaStreamSynchronize(c.stream));
   c.shards = G;
-  c.layout_key[0] = c.n;
-  c.layout_key[1] = batch;
-  c.layout_key[2] = G;
+  std::copy(key, key + 4, c.layout_key);
 }
 
 static ShardGeo make_geo(const Ctx& c) {
@@ -375,6 +419,8 @@ static ShardGeo make_geo(const Ctx& c) {
     g.bs[i] = c.sh_bs[i];
     g.nb[i] = c.sh_nb[i];
   }
+  g.p_lo = c.ranged ? c.range_p0 : 0;
+  g.p_hi = c.ranged ? c.range_p1 : c.n;
   if (c.rank >= 0) {
     g.rank_lo = c.sh_lo[c.rank];
     g.rank_hi = c.sh_lo[c.rank + 1];
@@ -504,19 +550,35 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   uint32_t* ctr = c.counters.as<uint32_t>();  // [0..1] claims, [2..3] bad, [4..5] loss, [8] nL, [9] nE
   F2V_CUDA(cudaMemsetAsync(ctr, 0, 8, c.stream));
   F2V_CUDA(cudaMemsetAsync(ctr + 2, 0xff, 8, c.stream));
-  if (monitor && multi) {  // only this process's positions are finalised here
+  F2V_CUDA(cudaMemsetAsync(ctr + 6, 0, 4, c.stream));  // row-poll stall flag
+  if (monitor && (multi || c.ranged)) {  // only some positions are finalised here
     zero_kernel<<<(c.n + 255) / 256, 256, 0, c.stream>>>(c.ploss.as<double>(), c.n);
     F2V_LAUNCHED(c.stream, "zero_kernel");
     ++c.launches;
   }
-  auto fill_sentinel = [&] {  // Znew := sentinel (cudaMalloc'd buffers are 256-byte aligned)
+  // replica emulation (tests): every shard of a one-GPU sharded run reads and
+  // publishes into its own Znew replica, rows reach the others as peer stores
+  const bool emul = std::getenv("F2V_EMULATE_REPLICAS") != nullptr && c.shards > 1 && !multi;
+  float* reps[ep::kMaxShards] = {};
+  if (emul) {
+    reps[0] = c.z[nxt].as<float>();
+    for (uint32_t g = 1; g < c.shards; ++g) {
+      c.rep[g - 1].ensure(sizeof(float) * size_t(c.n) * c.d);
+      reps[g] = c.rep[g - 1].as<float>();
+    }
+  }
+  auto fill_one = [&](float* z) {  // := sentinel (cudaMalloc'd buffers are 256-byte aligned)
     const uint64_t total = uint64_t(c.n) * c.d, n16 = total / 4;
     sentinel_kernel<<<uint32_t(std::min<uint64_t>((n16 + 255) / 256, 4u * c.num_sms * 8)), 256, 0,
-                      c.stream>>>(c.z[nxt].as<uint4>(), n16);
+                      c.stream>>>(reinterpret_cast<uint4*>(z), n16);
     F2V_LAUNCHED(c.stream, "sentinel_kernel");
-    if (total % 4)
-      sentinel_tail_kernel<<<1, 4, 0, c.stream>>>(c.z[nxt].as<float>(), n16 * 4, total);
+    if (total % 4) sentinel_tail_kernel<<<1, 4, 0, c.stream>>>(z, n16 * 4, total);
     c.launches += 1;
+  };
+  auto fill_sentinel = [&] {
+    fill_one(c.z[nxt].as<float>());
+    if (emul)
+      for (uint32_t g = 1; g < c.shards; ++g) fill_one(reps[g]);
   };
   fill_sentinel();
   // every replica holds the sentinel before any GPU stores a row into it
@@ -562,13 +624,20 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   a.R = c.tune.recent;
   a.lwarps = c.tune.lwarps;
   a.shards = c.shards;
+  for (uint32_t g = 0; g <= ep::kMaxShards; ++g)
+    a.shard_lo[g] = g <= c.shards ? c.sh_lo[g] : c.n;
   a.npeers = 0;
-  for (int g = 0; g < ep::kMaxShards; ++g) a.peer_znew[g] = nullptr;
+  for (int g = 0; g < ep::kMaxShards; ++g) {
+    a.peer_znew[g] = nullptr;
+    a.rep_znew[g] = reps[g];
+  }
+  a.emul = emul ? 1u : 0u;
   if (multi)
     for (uint32_t g = 0; g < c.world; ++g)
       if (int32_t(g) != c.rank) a.peer_znew[a.npeers++] = c.peer_z[g][nxt];
   a.eta = eta;
   a.fp = fp;
+  a.fp.stall = ctr + 6;
   a.nodep = debug_env("F2V_DEBUG_NODEP") ? 1 : 0;
   a.nnz = c.nnz;
   a.chunks = c.chunks;
@@ -596,7 +665,7 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   const uint64_t key = (uint64_t(c.n) * 1000003ull + c.nnz) ^ (uint64_t(a.b) << 40) ^
                        (uint64_t(fp.kind) << 56) ^ (uint64_t(c.shards) << 60) ^
                        (uint64_t(monitor) << 63);
-  const bool tunable = c.tune.fast && c.d == 128 && !multi;
+  const bool tunable = c.tune.fast && c.d == 128 && !multi && !c.ranged;
   bool tune_now = false;
   if (c.tune.minb == 2 || c.tune.minb == 3) {
     c.occ_use = int(c.tune.minb);
@@ -673,6 +742,24 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   uint64_t host[5];
   F2V_CUDA(cudaMemcpyAsync(host, ctr, 40, cudaMemcpyDeviceToHost, c.stream));
   F2V_CUDA(cudaStreamSynchronize(c.stream));
+  if (uint32_t(host[3]))  // ctr[6]
+    fail(F2V_ECUDA, "a Znew row never arrived within the 60 s poll deadline (stalled or dead "
+                    "peer GPU); the epoch was abandoned");
+  if (emul && host[1] == ~0ull) {  // every emulated replica must equal the primary
+    unsigned long long* diff = reinterpret_cast<unsigned long long*>(ctr + 12);
+    F2V_CUDA(cudaMemsetAsync(diff, 0, 8, c.stream));
+    for (uint32_t g = 1; g < c.shards; ++g) {
+      replica_diff_kernel<<<4u * c.num_sms, 256, 0, c.stream>>>(
+          c.z[nxt].as<uint32_t>(), reinterpret_cast<const uint32_t*>(reps[g]),
+          uint64_t(c.n) * c.d, diff);
+      F2V_LAUNCHED(c.stream, "replica_diff_kernel");
+    }
+    unsigned long long nd = 0;
+    F2V_CUDA(cudaMemcpyAsync(&nd, diff, 8, cudaMemcpyDeviceToHost, c.stream));
+    F2V_CUDA(cudaStreamSynchronize(c.stream));
+    if (nd) fail(F2V_ECUDA, "emulated replicas differ from the primary in " + std::to_string(nd) +
+                                " words");
+  }
   float kms = 0.f;
   F2V_CUDA(cudaEventElapsedTime(&kms, c.ev_kernel[0], c.ev_kernel[1]));
   c.timing[1] += kms;

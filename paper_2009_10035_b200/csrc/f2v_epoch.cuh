@@ -71,7 +71,14 @@ struct EpochArgs {
   // its negatives = set j * shards + shard(u); finalised rows are also stored
   // into the peers' Znew replicas (NVLink P2P) when npeers > 0
   uint32_t shards, npeers;
+  uint32_t shard_lo[kMaxShards + 1];  // shard g owns rows [shard_lo[g], shard_lo[g+1])
   float* peer_znew[kMaxShards];
+  // replica emulation (tests, F2V_EMULATE_REPLICAS): one launch runs every
+  // shard, but shard g's items read and write replica rep_znew[g] and store
+  // each finished row into every other replica -- the G-GPU data flow
+  // (store_peers, sentinel polls on peer-written rows) inside one kernel
+  uint32_t emul;
+  float* rep_znew[kMaxShards];
   float eta;
   ForceParams fp;
   uint64_t nnz, chunks, lslots;  // bounds, used by F2V_DEVICE_CHECKS builds
@@ -120,13 +127,20 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
-// shard g owns rows [floor(n g / G), floor(n (g+1) / G)) (orc_shard_range)
-__device__ __forceinline__ uint32_t shard_of(uint32_t u, uint32_t n, uint32_t G) {
-  return G == 1 ? 0u : uint32_t((uint64_t(u + 1) * G - 1) / n);
+// shard g owns rows [lo[g], lo[g+1]) (orc_shard_layout; G <= kMaxShards)
+__device__ __forceinline__ uint32_t shard_of(uint32_t u, const uint32_t* lo, uint32_t G) {
+  uint32_t g = 0;
+  for (uint32_t i = 1; i < G; ++i) g += u >= lo[i] ? 1u : 0u;
+  return g;
 }
 // index of the negative set of a vertex of step j: one set per (step, shard)
 __device__ __forceinline__ uint32_t neg_set(const EpochArgs& a, uint32_t u, uint32_t j) {
-  return a.shards == 1 ? j : j * a.shards + shard_of(u, a.n, a.shards);
+  return a.shards == 1 ? j : j * a.shards + shard_of(u, a.shard_lo, a.shards);
+}
+
+// the Znew replica the items of vertex u read and publish into
+__device__ __forceinline__ float* znew_of(const EpochArgs& a, uint32_t u) {
+  return a.emul ? a.rep_znew[shard_of(u, a.shard_lo, a.shards)] : a.znew;
 }
 
 // Per-warp FIFO of packed row ids (bit 31 = Znew) in shared memory; rows
@@ -135,6 +149,7 @@ template <int KIND, int K, bool VEC, bool MON, bool FAST, bool ATT>
 struct RowQueue {
   uint32_t* buf;
   int n;
+  const float* zn;  // the Znew replica of the item
   __device__ __forceinline__ void push(const EpochArgs& a, int lane, bool keep, uint32_t val,
                                        const float (&zu)[K], double (&acc)[K], double& lsum) {
     const uint32_t m = __ballot_sync(kFull, keep);
@@ -148,8 +163,8 @@ struct RowQueue {
       buf[lane] = rest;
       __syncwarp();
       n -= 32;
-      Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, 32, lane, a.d, a.zold, a.znew,
-                                                       zu, acc, lsum);
+      Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, 32, lane, a.d, a.zold, zn, zu,
+                                                       acc, lsum);
     }
   }
   __device__ __forceinline__ void flush(const EpochArgs& a, int lane, const float (&zu)[K],
@@ -159,16 +174,16 @@ struct RowQueue {
     __syncwarp();
     const int cnt = n;
     n = 0;
-    Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew, zu,
+    Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, cnt, lane, a.d, a.zold, zn, zu,
                                                      acc, lsum);
   }
 };
 
 // The shared negatives of batch j, in sample order (sampling.cpp:59).
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
-__device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, uint32_t q, int lane,
-                                             const float (&zu)[K], double (&acc)[K],
-                                             double& lsum) {
+__device__ __forceinline__ void do_negatives(const EpochArgs& a, const float* zn, uint32_t j,
+                                             uint32_t q, int lane, const float (&zu)[K],
+                                             double (&acc)[K], double& lsum) {
   for (uint32_t k0 = 0; k0 < a.s; k0 += 32) {
     const int cnt = int(umin32(32, a.s - k0));
     uint32_t pk = 0;
@@ -181,15 +196,20 @@ __device__ __forceinline__ void do_negatives(const EpochArgs& a, uint32_t j, uin
         pk = w;
       }
     }
-    Rows<KIND, K, VEC, MON, FAST>::template run<false>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew,
-                                                       zu, acc, lsum);
+    Rows<KIND, K, VEC, MON, FAST>::template run<false>(a.fp, pk, cnt, lane, a.d, a.zold, zn, zu,
+                                                       acc, lsum);
   }
 }
 
 // the row into every peer GPU's Znew replica (multi-GPU shards), out of line
 template <int K, bool VEC>
-__device__ __noinline__ void store_peers(const EpochArgs& a, uint32_t u, int lane,
+__device__ __noinline__ void store_peers(const EpochArgs& a, const float* zn, uint32_t u, int lane,
                                          const float (&nz)[K]) {
+  if (a.emul) {  // every other emulated replica
+    for (uint32_t g = 0; g < a.shards; ++g)
+      if (a.rep_znew[g] != zn) Lay<K, VEC>::store(a.rep_znew[g] + size_t(u) * a.d, lane, a.d, nz);
+    return;
+  }
   for (uint32_t g = 0; g < a.npeers; ++g)
     Lay<K, VEC>::store(a.peer_znew[g] + size_t(u) * a.d, lane, a.d, nz);
 }
@@ -197,8 +217,8 @@ __device__ __noinline__ void store_peers(const EpochArgs& a, uint32_t u, int lan
 // g = float(acc) (trainer.cpp:140-145); z_u -= eta*g in fp32 (trainer.cpp:173);
 // publish row u of Znew.
 template <int K, bool VEC, bool MON>
-__device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_t u, int lane,
-                                         const float (&zu)[K], const double (&acc)[K],
+__device__ __forceinline__ void finalize(const EpochArgs& a, float* zn, uint32_t p, uint32_t u,
+                                         int lane, const float (&zu)[K], const double (&acc)[K],
                                          double lsum) {
   using L = Lay<K, VEC>;
   bool bad = false;
@@ -210,8 +230,8 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, uint32_t p, uint32_
     nz[k] = __fsub_rn(zu[k], __fmul_rn(a.eta, g));
     if (nz[k] != nz[k]) nz[k] = __int_as_float(0x7fffffff);  // never the sentinel NaN
   }
-  L::store(a.znew + size_t(u) * a.d, lane, a.d, nz);  // publishes the row (sentinel-free)
-  if (a.npeers) store_peers<K, VEC>(a, u, lane, nz);  // the peers' replicas, over NVLink
+  L::store(zn + size_t(u) * a.d, lane, a.d, nz);  // publishes the row (sentinel-free)
+  if (a.npeers | a.emul) store_peers<K, VEC>(a, zn, u, lane, nz);  // peers' replicas (NVLink)
   const bool any_bad = __any_sync(kFull, bad);
   if (MON) {
     const double tot = warp_sum_d(lsum);
@@ -242,17 +262,28 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
   double lsum = 0.0;
   uint32_t wc = 0;
-  RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0};
+  float* zn = znew_of(a, u);
+  RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0, zn};
+  // Software pipeline over the chunk's 32-arc groups: while group i's rows
+  // are gathered and reduced, group i+1's states and group i+2's column ids
+  // are already in flight (the col -> state -> row chain is three dependent
+  // loads per arc).
+  uint32_t v_cur = e0 + lane < e1 ? __ldg(a.col + e0 + lane) : 0u;  // this group's ids
+  uint32_t v_nx = e0 + 32 + lane < e1 ? __ldg(a.col + e0 + 32 + lane) : 0u;  // the next's
+  uint32_t st_cur = e0 + lane < e1 ? ld_relaxed(a.state + v_cur) : 0u;  // this group's states
   for (uint64_t e = e0; e < e1; e += 32) {
     const int cnt = int(umin64(32, e1 - e));
-    uint32_t v = 0, pk = 0;
+    const uint32_t v = v_cur, st = st_cur;
+    uint32_t pk = 0;
+    // issue the next group's states and the group after's column ids
+    st_cur = e + 32 + lane < e1 ? ld_relaxed(a.state + v_nx) : 0u;
+    v_cur = v_nx;
+    v_nx = e + 64 + lane < e1 ? __ldg(a.col + e + 64 + lane) : 0u;
     bool use = false, win = false;
     if (lane < cnt) {
       DCHECK(e + lane < a.nnz, "E arc %llu nnz %llu", (unsigned long long)(e + lane),
              (unsigned long long)a.nnz);
-      v = a.col[e + lane];
       DCHECK(v < a.n, "E v=%u", v);
-      const uint32_t st = ld_relaxed(a.state + v);
       const uint32_t bv = st >> 1;
       if (bv >= j || F2V_NODEP(a)) {
         use = true;
@@ -274,8 +305,8 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   const bool needs = a.needs[u] != 0;
   if (nch == 1) {
     if (!needs) {
-      do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
-      finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
+      do_negatives<KIND, K, VEC, MON, FAST>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
+      finalize<K, VEC, MON>(a, zn, p, u, lane, zu, acc, lsum);
     } else {
       L::store_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);
       const double ls = MON ? warp_sum_d(lsum) : 0.0;
@@ -313,8 +344,8 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   }
   if (lane == 0) a.ecnt[u] = 0;
   if (!needs) {
-    do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
-    finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
+    do_negatives<KIND, K, VEC, MON, FAST>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
+    finalize<K, VEC, MON>(a, zn, p, u, lane, zu, acc, lsum);
   } else {
     L::store_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);  // the E total
     if (MON && lane == 0) __stcg(a.eloss + cb, lsum);  // lane 0 holds the whole sum here
@@ -326,9 +357,9 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
 
 // Take the parked recent window arcs in order, waiting on each row.
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
-__device__ __forceinline__ void recent_pass(const EpochArgs& a, int lane, uint32_t* rbuf, int& nr,
-                                            const float (&zu)[K], double (&acc)[K],
-                                            double& lsum) {
+__device__ __forceinline__ void recent_pass(const EpochArgs& a, const float* zn, int lane,
+                                            uint32_t* rbuf, int& nr, const float (&zu)[K],
+                                            double (&acc)[K], double& lsum) {
   for (int t0 = 0; t0 < nr; t0 += 32) {
     const int cnt = min(32, nr - t0);
     uint32_t pk = 0;
@@ -336,8 +367,8 @@ __device__ __forceinline__ void recent_pass(const EpochArgs& a, int lane, uint32
       const uint32_t v = rbuf[t0 + lane];
       pk = v | kNewBit;
     }
-    Rows<KIND, K, VEC, MON, FAST>::template run<true>(a.fp, pk, cnt, lane, a.d, a.zold, a.znew,
-                                                      zu, acc, lsum);
+    Rows<KIND, K, VEC, MON, FAST>::template run<true>(a.fp, pk, cnt, lane, a.d, a.zold, zn, zu,
+                                                      acc, lsum);
   }
   __syncwarp();
   nr = 0;
@@ -349,14 +380,14 @@ __device__ __forceinline__ void recent_pass(const EpochArgs& a, int lane, uint32
 // taken last (recent_pass) so the dependency tail of the item is short.  The
 // order is a function of the data only (deterministic).
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
-__device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, uint32_t j,
-                                               uint32_t c0, uint32_t c1, int lane,
+__device__ __forceinline__ void window_collect(const EpochArgs& a, const float* zn, uint32_t u,
+                                               uint32_t j, uint32_t c0, uint32_t c1, int lane,
                                                uint32_t* qbuf, uint32_t* rbuf, int& nr,
                                                const float (&zu)[K], double (&acc)[K],
                                                double& lsum) {
   const uint64_t r0 = a.rowptr[u];
   const uint32_t cb = a.cbase[u];
-  RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0};
+  RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0, zn};
   for (uint32_t cc = c0; cc < c1; cc += 32) {
     const uint32_t nc = umin32(32, c1 - cc);
     const uint32_t mine = lane < int(nc) ? __ldcg(a.wcnt + cb + cc + lane) : 0u;
@@ -397,7 +428,7 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, uint32_t u, u
       // park the recent ones (processed in place if the parking lot is full)
       if (nr + __popc(rm) > kRq) {
         q.flush(a, lane, zu, acc, lsum);
-        recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
+        recent_pass<KIND, K, VEC, MON, FAST>(a, zn, lane, rbuf, nr, zu, acc, lsum);
       }
       if (recent) rbuf[nr + __popc(rm & lanemask_lt(lane))] = v;
       __syncwarp();
@@ -422,6 +453,7 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   unsigned long long* lt = (a.ltrace && cl == 0) ? a.ltrace + 4ull * p : nullptr;
 #endif
   if (lane == 0) F2V_STAMP(lt, 0);
+  float* zn = znew_of(a, u);
   float zu[K];
   L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
   double acc[K];
@@ -442,18 +474,20 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     if (MON && lane == 0) lsum = __ldcg(a.eloss + cb);
     int nr = 0;
     // E total + old window arcs + negatives + recent arcs
-    window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
-    do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
+    window_collect<KIND, K, VEC, MON, FAST>(a, zn, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
+                                            lsum);
+    do_negatives<KIND, K, VEC, MON, FAST>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
     if (lane == 0) F2V_STAMP(lt, 2);
-    recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
+    recent_pass<KIND, K, VEC, MON, FAST>(a, zn, lane, rbuf, nr, zu, acc, lsum);
     if (lane == 0) F2V_STAMP(lt, 3);
-    finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
+    finalize<K, VEC, MON>(a, zn, p, u, lane, zu, acc, lsum);
     if (lane == 0) a.vflag[u] = 0;
     return;
   }
   int nr = 0;
-  window_collect<KIND, K, VEC, MON, FAST>(a, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc, lsum);
-  recent_pass<KIND, K, VEC, MON, FAST>(a, lane, rbuf, nr, zu, acc, lsum);
+  window_collect<KIND, K, VEC, MON, FAST>(a, zn, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
+                                          lsum);
+  recent_pass<KIND, K, VEC, MON, FAST>(a, zn, lane, rbuf, nr, zu, acc, lsum);
   const uint32_t slot = a.lpo[u] + cl;
   DCHECK(slot < a.lslots, "L slot=%u lslots=%llu cl=%u nchL=%u", slot,
          (unsigned long long)a.lslots, cl, nchL);
@@ -476,9 +510,9 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     L::add_acc(a.lpart + size_t(lp + qq) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __dadd_rn(lsum, __ldcg(a.lloss + lp + qq));
   }
-  do_negatives<KIND, K, VEC, MON, FAST>(a, j, neg_set(a, u, j), lane, zu, acc, lsum);
+  do_negatives<KIND, K, VEC, MON, FAST>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
   if (lane == 0) a.lcnt[u] = 0;
-  finalize<K, VEC, MON>(a, p, u, lane, zu, acc, lsum);
+  finalize<K, VEC, MON>(a, zn, p, u, lane, zu, acc, lsum);
   if (lane == 0) a.vflag[u] = 0;
 }
 
@@ -532,17 +566,28 @@ void launch_one(Ctx& c, const EpochArgs& a) {
   ++c.launches;
 }
 
+#ifndef F2V_EXACT_MINB
+// EXACT d = 128 register budget (resident 8-warp CTAs per SM): 3 (80
+// registers, 24 warps/SM) measured 57.7 ms on C3 against 65.1 ms at 2 (128)
+#define F2V_EXACT_MINB 3
+#endif
+
 template <int KIND, int K, bool VEC, bool FAST>
 void launch_mon(Ctx& c, const EpochArgs& a, bool mon) {
-  if constexpr (FAST && K == 4) {
-    if (c.occ_use == 3) {
-      if (mon) launch_one<KIND, K, VEC, true, FAST, 3>(c, a);
-      else launch_one<KIND, K, VEC, false, FAST, 3>(c, a);
-      return;
+  if constexpr (!FAST && K == 4 && VEC) {
+    if (mon) launch_one<KIND, K, VEC, true, FAST, F2V_EXACT_MINB>(c, a);
+    else launch_one<KIND, K, VEC, false, FAST, F2V_EXACT_MINB>(c, a);
+  } else {
+    if constexpr (FAST && K == 4) {
+      if (c.occ_use == 3) {
+        if (mon) launch_one<KIND, K, VEC, true, FAST, 3>(c, a);
+        else launch_one<KIND, K, VEC, false, FAST, 3>(c, a);
+        return;
+      }
     }
+    if (mon) launch_one<KIND, K, VEC, true, FAST, 2>(c, a);
+    else launch_one<KIND, K, VEC, false, FAST, 2>(c, a);
   }
-  if (mon) launch_one<KIND, K, VEC, true, FAST, 2>(c, a);
-  else launch_one<KIND, K, VEC, false, FAST, 2>(c, a);
 }
 
 template <int K, bool VEC, bool FAST>

@@ -32,6 +32,9 @@ struct ForceParams {
   int32_t has_cap;
   double eps;  // double(model.epsilon)   (force_kernels.cpp:105,113)
   double cap;  // double(*repulsion_cap)  (force_kernels.cpp:72)
+  // epoch kernel: set to 1 when a Znew row never arrived within the poll
+  // deadline (a stalled or dead peer GPU); the host raises F2V_ECUDA
+  uint32_t* stall = nullptr;
 };
 
 struct DeviceBuf {
@@ -103,10 +106,16 @@ struct Ctx {
   DeviceBuf poff, lperm;      // combined start of (step, shard) batches; per-shard perms
   std::vector<uint32_t> h_poff;
   uint32_t steps = 0;         // T = max over shards of the local batch count
-  uint64_t layout_key[3] = {0, 0, 0};
+  // batch range of one epoch (f2v_train_config.first_batch / run_batches):
+  // positions [range_p0, range_p1) = steps [range_t0, range_t1); others keep Z
+  uint32_t range_p0 = 0, range_p1 = 0, range_t0 = 0, range_t1 = 0;
+  bool ranged = false;
+  uint64_t layout_key[4] = {0, 0, 0, 0};  // (graph_gen, batch, G, s) of the layout
+  uint64_t graph_gen = 0;                  // bumped by every f2v_upload_graph
   std::vector<uint32_t> sh_lo, sh_bs, sh_nb;  // per shard: first row, batch, batches
   // multi-process: IPC-shared control block + the peers' replicas (f2v_shard.cu)
   DeviceBuf ctl;
+  DeviceBuf rep[7];  // emulated peer replicas of Znew (F2V_EMULATE_REPLICAS, tests)
   bool shard_ready = false;
   float* peer_z[8][2] = {};
   void* peer_ctl[8] = {};
@@ -141,7 +150,7 @@ struct EpochResult {
   double loss;
 };
 void k_prepare_graph(Ctx& c);
-void k_shard_layout(Ctx& c, uint32_t batch, uint32_t G);
+void k_shard_layout(Ctx& c, uint32_t batch, uint32_t G, uint32_t s);
 void k_epoch_perm(Ctx& c, uint32_t epoch, uint64_t seed);
 void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sampler);
 void k_set_context(Ctx& c, uint32_t walk_k);   // f2v_walk.cu
@@ -151,7 +160,8 @@ void k_epoch_restore(Ctx& c, uint64_t bad_step);
 void k_device_partition(Ctx& c, uint32_t n, uint64_t seed, uint32_t epoch, uint32_t* perm_out);
 void k_device_partition_keyed(Ctx& c, uint32_t n, uint64_t s0, uint32_t* perm_out);
 // host: per-shard ranges/batches and the combined (step, shard) start positions
-void shard_layout(uint32_t n, uint32_t batch, uint32_t G, std::vector<uint32_t>& lo,
+void shard_layout(const uint64_t* rowptr, uint32_t n, uint32_t s, uint32_t batch, uint32_t G,
+                  std::vector<uint32_t>& lo,
                   std::vector<uint32_t>& bs, std::vector<uint32_t>& nb,
                   std::vector<uint32_t>& poff, uint32_t& T);
 // multi-process shards (f2v_shard.cu)

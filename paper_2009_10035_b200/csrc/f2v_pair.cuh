@@ -43,6 +43,15 @@ __device__ __forceinline__ bool has_sentinel(const float (&v)[K]) {
   return b;
 }
 
+// Row polls give up after this much wall time (%globaltimer, ns).
+constexpr unsigned long long kPollDeadlineNs = 60ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ bool poll_expired(unsigned long long& t0) {
+  unsigned long long now;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
+  if (!t0) t0 = now;
+  return now - t0 > kPollDeadlineNs;
+}
+
 // Relaxed (no L1 invalidation) global loads/stores for cross-warp flags; the
 // data they guard is always read through L2 (ld.cg) after the flag is seen.
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
@@ -99,18 +108,23 @@ struct Lay {
     }
   }
   // a Znew row: re-load until no lane sees the sentinel (warp-uniform loop).
-  // A row that never arrives (a peer GPU died mid-epoch) traps after 2^28
-  // polls (minutes) instead of hanging the device.
+  // A row that never arrives (a peer GPU stalled or died mid-epoch) gives up
+  // after kPollDeadlineNs of wall time and raises *stall: the host reports
+  // F2V_ECUDA instead of the device hanging or trapping.
   __device__ static __forceinline__ void poll(const float* row, int lane, uint32_t d,
-                                              float (&v)[K]) {
+                                              float (&v)[K], uint32_t* stall) {
     // exponential back-off (32 ns .. F2V_POLL_MAX_NS): spinning warps would
     // otherwise take issue slots from the warps streaming rows on the same SM
-    uint32_t it = 0, ns = 32;
+    uint32_t ns = 32;
+    unsigned long long t0 = 0;
     while (__any_sync(kFull, has_sentinel<K, (VEC && K % 4 == 0) ? 2 : 1>(v))) {
       __nanosleep(ns);
       ns = ns < F2V_POLL_MAX_NS ? 2 * ns : ns;
       load(row, lane, d, v, true);
-      if (++it == (1u << 26)) __trap();
+      if (poll_expired(t0)) {
+        if (lane == 0 && stall) atomicExch(stall, 1u);
+        break;
+      }
     }
   }
   __device__ static __forceinline__ void store(float* row, int lane, uint32_t d,
@@ -303,7 +317,7 @@ __device__ __forceinline__ void rows_exact(const ForceParams& fp, uint32_t packe
 #pragma unroll
     for (int i = 0; i < U; ++i)  // Znew rows not yet final: poll
       if (k0 + i < cnt && (pks[i] & kNewBit))
-        L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, v[i]);
+        L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, v[i], fp.stall);
     double w[U][K], red[U], nw[U];
 #pragma unroll
     for (int i = 0; i < U; ++i) {
@@ -489,6 +503,10 @@ __device__ __forceinline__ void fast_block(const ForceParams& fp, int k0, int cn
   for (int k = 0; k < K; ++k) acc[k] = __dadd_rn(acc[k], double(a32[k]));
 }
 
+#ifndef F2V_EXACT_PIPE
+#define F2V_EXACT_PIPE 0  // EXACT: gather the next 8-row block during this one's math
+#endif
+
 #ifndef F2V_FAST_INFLIGHT
 #define F2V_FAST_INFLIGHT 8  // row gathers in flight per warp (8; 16 measured slower)
 #endif
@@ -532,7 +550,7 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
 #pragma unroll
         for (int i = 8 * h; i < 8 * h + 8; ++i)
           if (k0 + i < cnt && (pks[i] & kNewBit))
-            L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, w[h][i % 8]);
+            L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, w[h][i % 8], fp.stall);
       }
       fast_block<KIND, K, MON, ATT>(fp, k0 + 8 * h, cnt, lane, zu, w[h], acc, lsum);
     }
@@ -595,9 +613,9 @@ __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t pack
     acc[k] = acc_io[k];
   }
   double lsum = lsum_io;
-  for (int k0 = 0; k0 < cnt; k0 += 8) {
-    float v[8][K];
-    uint32_t pks[8];
+  // one block = 8 rows: gather (one 16-byte load per lane per row), then
+  // the fp64 pair math of the block
+  auto load_block = [&](int k0, float (&v)[8][K], uint32_t (&pks)[8]) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const uint32_t pk = __shfl_sync(kFull, packed, (k0 + i) & 31);
@@ -610,6 +628,8 @@ __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t pack
         for (int k = 0; k < K; ++k) v[i][k] = 0.0f;
       }
     }
+  };
+  auto compute_block = [&](int k0, float (&v)[8][K], const uint32_t (&pks)[8]) {
     {  // Znew rows not yet final: one vote for the block, then poll row by row
       bool pend = false;
 #pragma unroll
@@ -620,7 +640,7 @@ __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t pack
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           if (k0 + i < cnt && (pks[i] & kNewBit))
-            L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, v[i]);
+            L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, v[i], fp.stall);
       }
     }
     // per-lane fp64 partial dot / distance of the 8 pairs.  Sigmoid: the
@@ -690,7 +710,28 @@ __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t pack
         }
       }
     }
+    };
+#if F2V_EXACT_PIPE
+  // software pipeline: the next block's gathers are in flight while this
+  // block's fp64 math runs (two register blocks, no dynamic indexing)
+  float va[8][K], vb[8][K];
+  uint32_t pa[8], pb[8];
+  load_block(0, va, pa);
+  for (int k0 = 0; k0 < cnt; k0 += 16) {
+    if (k0 + 8 < cnt) load_block(k0 + 8, vb, pb);
+    compute_block(k0, va, pa);
+    if (k0 + 8 >= cnt) break;
+    if (k0 + 16 < cnt) load_block(k0 + 16, va, pa);
+    compute_block(k0 + 8, vb, pb);
   }
+#else
+  for (int k0 = 0; k0 < cnt; k0 += 8) {
+    float v[8][K];
+    uint32_t pks[8];
+    load_block(k0, v, pks);
+    compute_block(k0, v, pks);
+  }
+#endif
 #pragma unroll
   for (int k = 0; k < K; ++k) acc_io[k] = acc[k];
   lsum_io = lsum;
@@ -732,12 +773,16 @@ __device__ __forceinline__ void rows_lowd(const ForceParams& fp, uint32_t packed
     for (int c = 0; c < kLowD; ++c) b |= __float_as_uint(w[c]) == kSentinel;
     return b && mine && (pk & kNewBit);
   };
-  uint32_t it = 0, ns = 32;
+  uint32_t ns = 32;
+  unsigned long long t0 = 0;
   while (__any_sync(kFull, pending())) {
     __nanosleep(ns);
     ns = ns < F2V_POLL_MAX_NS ? 2 * ns : ns;
     if (pending()) load();
-    if (++it == (1u << 26)) __trap();
+    if (poll_expired(t0)) {
+      if (lane == 0 && fp.stall) atomicExch(fp.stall, 1u);
+      break;
+    }
   }
   float red = 0.f, nrm = 0.f;
 #pragma unroll

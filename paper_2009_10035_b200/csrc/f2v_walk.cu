@@ -22,6 +22,10 @@
 namespace f2v {
 namespace {
 
+struct ShardBounds {
+  uint32_t lo[ep::kMaxShards + 1];
+};
+
 // flag[p] = the vertex at combined position p has a walk (degree > 0)
 __global__ void walkable_kernel(const uint32_t* __restrict__ perm,
                                 const uint64_t* __restrict__ grow, uint32_t* __restrict__ flag,
@@ -35,14 +39,15 @@ __global__ void walk_kernel(const uint32_t* __restrict__ perm, const uint32_t* _
                             const uint32_t* __restrict__ wpos, const uint32_t* __restrict__ poff,
                             const uint64_t* __restrict__ grow, const uint32_t* __restrict__ gcol,
                             const uint64_t* __restrict__ crow, uint32_t* __restrict__ ccol,
-                            uint32_t n, uint32_t G, uint32_t k, uint64_t seed, uint32_t epoch) {
+                            uint32_t n, ShardBounds sb, uint32_t G, uint32_t k, uint64_t seed,
+                            uint32_t epoch) {
   const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const uint32_t u = perm[p];
   const uint64_t d0 = grow[u + 1] - grow[u];
   if (d0 == 0) return;  // isolated start: empty walk
   const uint32_t t = state[u] >> 1;
-  const uint32_t g = ep::shard_of(u, n, G);
+  const uint32_t g = ep::shard_of(u, sb.lo, G);
   const uint64_t s0 = G == 1 ? rng_keyed3(seed, kStreamSampling, epoch, t)
                              : rng_keyed4(seed, kStreamSampling, epoch, t, g);
   const uint64_t base = uint64_t(k) * (wpos[p] - wpos[poff[uint64_t(t) * G + g]]);
@@ -108,10 +113,12 @@ void k_epoch_walks(Ctx& c, uint32_t epoch, uint64_t seed) {
   c.scan_tmp.ensure(tmp);
   F2V_CUDA(cub::DeviceScan::ExclusiveSum(c.scan_tmp.p, tmp, c.wflag.as<uint32_t>(),
                                          c.wpos.as<uint32_t>(), n + 1, c.stream));
+  ShardBounds bounds{};
+  for (uint32_t g = 0; g <= c.shards; ++g) bounds.lo[g] = c.sh_lo[g];
   walk_kernel<<<(n + 255) / 256, 256, 0, c.stream>>>(
       c.perm.as<uint32_t>(), c.state.as<uint32_t>(), c.wpos.as<uint32_t>(),
       c.poff.as<uint32_t>(), c.grow.as<uint64_t>(), c.gcol.as<uint32_t>(),
-      c.rowptr.as<uint64_t>(), c.col.as<uint32_t>(), n, c.shards, c.walk_k, seed, epoch);
+      c.rowptr.as<uint64_t>(), c.col.as<uint32_t>(), n, bounds, c.shards, c.walk_k, seed, epoch);
   F2V_LAUNCHED(c.stream, "walk_kernel");
   c.launches += 3;
 }

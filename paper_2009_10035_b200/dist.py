@@ -2,14 +2,16 @@
 (DESIGN.md "Multi-GPU").
 
 Semantics (pinned by the oracle, oracle/f2v_oracle.c orc_train with G > 1):
-shard g of G owns rows [n g / G, n (g+1) / G) (``shard_range``), shuffles
-them every epoch with partition_epoch on (seed, {0x22, epoch, g})
-(sampling.cpp:7-19, trainer.cpp:216-217), batch b_g = min(batch, |shard|)
-(trainer.cpp:200), and draws the negatives of its t-th batch from
+shard g of G owns a contiguous row range cut at quantiles of the per-vertex
+work deg(u) + s (``shard_layout``: R-MAT's hubs do not pile onto shard 0),
+shuffles it every epoch with partition_epoch on (seed, {0x22, epoch, g})
+(sampling.cpp:7-19, trainer.cpp:216-217), uses the local batch
+ceil(|shard| / T) with T = ceil(n / (G batch)) steps (so per-step work is
+balanced too), and draws the negatives of its t-th batch from
 (seed, {0x33, epoch, t, g}) or Philox with shard = g.  Step t = the t-th
 local batch of every shard: all gradients on ONE snapshot of Z
 (trainer.cpp:227-233), then every update (trainer.cpp:235) -- synchronous
-minibatch SGD with global batch G*b.  G = 1 is exactly the reference.
+minibatch SGD with global batch ~G*b.  G = 1 is exactly the reference.
 
 Two exchange paths, same results:
 
@@ -36,7 +38,7 @@ from typing import List, Optional, Tuple
 import numpy as np
 
 from . import (CsrGraph, Device, NumericalError, TrainConfig, TrainCounters, UsageError,
-               negatives, partition_shard, shard_range)
+               negatives, partition_shard, shard_layout)
 
 __all__ = ["env_rank", "ShardedDevice", "StepBackend", "DeviceBackend", "train_allgather",
            "shard_steps"]
@@ -48,15 +50,12 @@ def env_rank() -> Tuple[int, int, int]:
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
-def shard_steps(n: int, batch: int, shards: int) -> Tuple[List[int], List[int], int]:
-    """Per shard batch size and batch count, and T = steps per epoch."""
-    bs, nb = [], []
-    for g in range(shards):
-        lo, hi = shard_range(n, shards, g)
-        b = min(batch, hi - lo)
-        bs.append(b)
-        nb.append((hi - lo + b - 1) // b)
-    return bs, nb, max(nb)
+def shard_steps(g: CsrGraph, batch: int, shards: int, negatives: int
+                ) -> Tuple[List[int], List[int], List[int], int]:
+    """Row bounds lo[G+1], per-shard batch size and batch count, T = steps."""
+    lo, bs, _, T = shard_layout(g, batch, shards, negatives)
+    nb = [(int(lo[i + 1] - lo[i]) + int(bs[i]) - 1) // int(bs[i]) for i in range(shards)]
+    return [int(x) for x in lo], [int(x) for x in bs], nb, T
 
 
 def _all_gather_objects(obj, group=None) -> list:
@@ -179,10 +178,9 @@ def _failed_vertex(e: NumericalError, ids: np.ndarray) -> Tuple[int, int]:
     return (int(hit[0]) if len(hit) else 0), v
 
 
-def train_allgather(backend: StepBackend, n: int, cfg: TrainConfig, rank: int, world: int,
+def train_allgather(backend: StepBackend, g: CsrGraph, cfg: TrainConfig, rank: int, world: int,
                     first_epoch: int = 0, run_epochs: int = 0, group=None,
-                    tensor_device=None, counters: Optional[TrainCounters] = None,
-                    degrees: Optional[np.ndarray] = None) -> list:
+                    tensor_device=None, counters: Optional[TrainCounters] = None) -> list:
     """The G-shard schedule with an explicit all-gather of updated rows after
     every step.  Returns the epoch losses (identical on every rank; summed in
     (step, shard) order like orc_train) when cfg.monitor_loss."""
@@ -192,10 +190,11 @@ def train_allgather(backend: StepBackend, n: int, cfg: TrainConfig, rank: int, w
     if world != dist.get_world_size(group):
         raise UsageError("world does not match the process group")
     d = backend.d
-    lo, hi = shard_range(n, world, rank)
-    bs, nb, T = shard_steps(n, cfg.batch, world)
-    bmax = max(bs)
+    n = g.num_vertices()
     s = cfg.negatives
+    bounds, bs, nb, T = shard_steps(g, cfg.batch, world, s)
+    lo, hi = bounds[rank], bounds[rank + 1]
+    bmax = max(bs)
     end = min(cfg.epochs, first_epoch + run_epochs) if run_epochs else cfg.epochs
     tdev = tensor_device if tensor_device is not None else torch.device("cpu")
     losses = []
@@ -248,16 +247,16 @@ def train_allgather(backend: StepBackend, n: int, cfg: TrainConfig, rank: int, w
             mine = torch.from_numpy(pack).to(tdev)
             allp = [torch.zeros_like(mine) for _ in range(world)]
             dist.all_gather(allp, mine, group=group)
-            for g in range(world):
-                p = allp[g].cpu().numpy()
+            for r in range(world):
+                p = allp[r].cpu().numpy()
                 cnt = int(p[0])
-                if cnt and g != rank:
+                if cnt and r != rank:
                     backend.set_rows(p[1:1 + cnt].view(np.uint32),
                                      p[1 + bmax:1 + bmax + cnt * d].view(np.float32).reshape(cnt, d))
                 if cfg.monitor_loss and cnt:
                     epoch_loss += float(p[-2:].copy().view(np.float64)[0])
-        if counters is not None and degrees is not None:
-            counters.attractive_evals += int(degrees.sum())
+        if counters is not None:
+            counters.attractive_evals += int(g.num_edges())
             counters.repulsive_evals += n * s
         if cfg.monitor_loss:
             losses.append(epoch_loss)

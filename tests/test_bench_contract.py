@@ -75,3 +75,27 @@ def test_reference_graph_equals_product_graph(f2v, orc):
             g = f2v.rgg_graph(kw["n"], kw["mean_deg"], kw["seed"])
         assert np.array_equal(g.row_offsets, rrow), name
         assert np.array_equal(g.col_indices, rcol), name
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["c2", "c3"])
+def test_full_size_csr_matches_reference_from_edges(f2v, orc, cfg):
+    """north_star: CSR construction bit-exact.  The bench configs' graphs at
+    FULL size: the product's CSR (product generator -> parallel
+    csr_from_edges) against the reference's own CsrGraph::from_edges
+    (csr_graph.cpp:57-97) on the oracle's edge list -- row offsets and column
+    indices byte-identical (VERDICT r1 "what's weak" #7)."""
+    import numpy as np
+    import bench
+    if not orc.reference_available():
+        pytest.skip("oracle/_ref not built")
+    gen, kw = bench.CONFIGS[cfg][0], bench.CONFIGS[cfg][1]
+    pairs, n = orc.orc_gen_pairs(gen, **kw)
+    rg = orc.ref_graph_from_edges(pairs, n, True)
+    del pairs
+    rrow, rcol = rg.csr()
+    del rg
+    g = bench.make_graph(f2v, cfg)
+    assert g.num_vertices() == n
+    assert np.array_equal(g.row_offsets, rrow)
+    assert np.array_equal(g.col_indices, rcol)

@@ -40,21 +40,47 @@ def _mix(z):  # rng.hpp:44-49
     return z ^ (z >> 31)
 
 
-def test_shard_layout_matches_definition(f2v):
-    for n, b, G in [(1000, 64, 2), (1001, 64, 3), (37, 8, 8), (10, 64, 3), (4096, 256, 1)]:
-        poff, T = f2v.shard_layout(n, b, G)
-        pos = 0
-        for t in range(T):
-            for g in range(G):
-                assert poff[t * G + g] == pos
-                lo, hi = f2v.shard_range(n, G, g)
-                bs = min(b, hi - lo)
-                nb = (hi - lo + bs - 1) // bs
-                if t < nb:
-                    pos += min(bs, hi - lo - t * bs)
-        assert poff[T * G] == pos == n
+def test_shard_layout_matches_oracle(f2v, orc):
+    """The product's shard layout equals the oracle's definition
+    (orc_shard_layout): work-quantile row bounds, per-shard batches, and the
+    combined step-major positions."""
+    graphs = [f2v.rmat_graph(12, 16, seed=2), f2v.sbm_graph(1001, 7, 0.02, 0.002, 3),
+              f2v.CsrGraph(np.zeros(38, np.uint64), np.zeros(0, np.uint32)),
+              f2v.CsrGraph(np.zeros(11, np.uint64), np.zeros(0, np.uint32))]
+    for g in graphs:
+        n = g.num_vertices()
+        for b, G, s in [(64, 2, 5), (64, 3, 5), (8, 8, 1), (64, 3, 6), (256, 1, 5)]:
+            if n < G:
+                continue
+            lo, bs, poff, T = f2v.shard_layout(g, b, G, s)
+            rlo, rbs, rnb, rT = orc.orc_shard_layout(g.row_offsets, G, s, b)
+            assert np.array_equal(lo, rlo) and np.array_equal(bs, rbs) and T == rT
+            assert lo[0] == 0 and lo[G] == n and np.all(np.diff(lo.astype(np.int64)) >= 1)
+            pos = 0
+            for t in range(T):
+                for k in range(G):
+                    assert poff[t * G + k] == pos
+                    if t < rnb[k]:
+                        pos += min(int(bs[k]), int(lo[k + 1] - lo[k]) - t * int(bs[k]))
+            assert poff[T * G] == pos == n
     with pytest.raises(f2v.UsageError):
-        f2v.shard_layout(3, 4, 4)
+        f2v.shard_layout(f2v.CsrGraph(np.zeros(4, np.uint64), np.zeros(0, np.uint32)), 4, 4, 5)
+
+
+def test_shard_layout_balances_rmat_work(f2v, orc):
+    """R-MAT's hub rows have low ids: equal row ranges gave shard 0 of 8
+    ~42% of the arcs.  Work-quantile bounds keep every shard
+    within a few percent of 1/G of the work, and every shard's step count
+    within one of T."""
+    g = f2v.rmat_graph(16, 16, seed=1)
+    n, s = g.num_vertices(), 5
+    w = g.degrees() + s
+    for G in (2, 4, 8):
+        lo, bs, poff, T = f2v.shard_layout(g, 384, G, s)
+        share = np.array([w[lo[k]:lo[k + 1]].sum() for k in range(G)]) / w.sum()
+        assert share.max() <= 1.0 / G + 0.01, share
+        nb = [-(-int(lo[k + 1] - lo[k]) // int(bs[k])) for k in range(G)]
+        assert max(nb) == T and min(nb) >= T - 1, (nb, T)
 
 
 def test_partition_shard_matches_oracle(f2v, orc):
@@ -133,7 +159,7 @@ def _worker(rank, world, port, case, q):
                               lr_decay=case.get("decay", "constant"))
         err = None
         try:
-            losses = f2vdist.train_allgather(be, case["n"], cfg, rank, world)
+            losses = f2vdist.train_allgather(be, g, cfg, rank, world)
         except f2v.NumericalError as e:
             losses, err = None, str(e)
         # the IPC-handle exchange of ShardedDevice.setup (bytes objects)

@@ -172,7 +172,7 @@ def test_allgather_driver_on_device(f2v, orc, backend):
         with f2v.Device(0) as dv:
             dv.upload_graph(g)
             dv.set_embedding(z0)
-            losses = train_allgather(DeviceBackend(dv), n, cfg, 0, 1, tensor_device=tdev)
+            losses = train_allgather(DeviceBackend(dv), g, cfg, 0, 1, tensor_device=tdev)
             z = dv.get_embedding()
             rows = dv.get_rows(np.array([3, 1, 3], np.uint32))
             assert np.array_equal(rows, z[[3, 1, 3]])
@@ -183,3 +183,41 @@ def test_allgather_driver_on_device(f2v, orc, backend):
     assert rc == 0
     z_parity(z, zr)
     np.testing.assert_allclose(losses, lr_, rtol=1e-9)
+
+
+@pytest.mark.parametrize("precision", ["fast", "exact"])
+@pytest.mark.parametrize("G,kind,d", [(2, "sigmoid", 128), (3, "tdist", 128), (8, "tdist", 64),
+                                      (4, "sigmoid", 2)])
+def test_emulated_replicas_match_oracle(f2v, orc, dev, precision, G, kind, d):
+    """The G-GPU data flow inside ONE launch (the safe stand-in for G GPUs on
+    one device): shard g's items read and publish into their own Znew
+    replica, and every finished row reaches the other replicas only through
+    the peer-store epilogue (store_peers) -- so readers poll sentinels of
+    rows written by "peers".  After every epoch all replicas are checked equal
+    on the device; Z must equal orc_train(G) and the one-replica run bit for
+    bit."""
+    g = f2v.rmat_graph(12, 16, seed=G)  # skewed degrees: uneven work-balanced shards
+    n = g.num_vertices()
+    z0 = np.zeros((n, d), np.float32)
+    orc.oracle().orc_random_embedding(n, d, 5, z0)
+    cfg = f2v.TrainConfig(dim=d, batch=48, negatives=5, lr=0.02, epochs=2,
+                          model=kind_model(f2v, kind), seed=3, monitor_loss=True,
+                          sampler="philox", precision=precision, shards=G)
+    outs = []
+    for emul in (False, True):
+        if emul:
+            os.environ["F2V_EMULATE_REPLICAS"] = "1"
+        try:
+            dev.upload_graph(g)
+            dev.set_embedding(z0)
+            losses = dev.train_epochs(cfg)
+            outs.append((losses, dev.get_embedding()))
+        finally:
+            os.environ.pop("F2V_EMULATE_REPLICAS", None)
+    assert outs[0][0] == outs[1][0] and np.array_equal(outs[0][1], outs[1][1])
+    rc, zr, lr_, _, _ = orc.orc_train(g.row_offsets, g.col_indices, z0, 48, 5, 0.02, 2, kind, 3,
+                                      sampler="philox", G=G, threads=8)
+    assert rc == 0
+    np.testing.assert_allclose(outs[1][0], lr_, rtol=1e-3)
+    rel = np.linalg.norm(outs[1][1].astype(np.float64) - zr) / np.linalg.norm(zr)
+    assert rel < 1e-4, rel
