@@ -239,6 +239,16 @@ int32_t f2v_shard_handle_bytes(void);
 int32_t f2v_shard_init(f2v_ctx* ctx, uint32_t rank, uint32_t world);
 int32_t f2v_shard_export(f2v_ctx* ctx, uint8_t* handles_out);
 int32_t f2v_shard_attach(f2v_ctx* ctx, const uint8_t* all_handles);
+/* Per-step all-gather baseline (SURVEY §8e ladder step 1): the same G-shard
+ * schedule, with each step's updated rows exchanged by ncclAllGather over
+ * NVLink (NCCL loaded at run time, libnccl.so.2).  One process per GPU:
+ * rank 0 calls f2v_nccl_unique_id, the caller broadcasts the 128 bytes, every
+ * rank calls f2v_nccl_init, then f2v_train_epochs_allgather (cfg.shards 0 or
+ * world).  Same results as f2v_train_epochs on an attached context. */
+int32_t f2v_nccl_unique_id(uint8_t* unique_id_out /* 128 bytes */);
+int32_t f2v_nccl_init(f2v_ctx* ctx, const uint8_t* unique_id, uint32_t rank, uint32_t world);
+int32_t f2v_train_epochs_allgather(f2v_ctx* ctx, const f2v_train_config* cfg, double* loss_out,
+                                   f2v_counters* counters, f2v_failure* failure);
 /* rows of the device Z by id (the per-step all-gather driver, dist.py):
  * rows f32[b*d] row-major */
 int32_t f2v_get_rows(f2v_ctx* ctx, const uint32_t* ids, uint32_t b, float* rows_out);

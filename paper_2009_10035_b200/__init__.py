@@ -157,6 +157,10 @@ SYMBOLS = {
     "f2v_shard_attach": (_i32, [_vp, C.c_char_p]),
     "f2v_partition_shard": (_i32, [C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
                                    C.c_uint32, _u32p]),
+    "f2v_nccl_unique_id": (_i32, [C.c_char_p]),
+    "f2v_nccl_init": (_i32, [_vp, C.c_char_p, C.c_uint32, C.c_uint32]),
+    "f2v_train_epochs_allgather": (_i32, [_vp, C.POINTER(_TrainConfig), _vp, C.POINTER(_Counters),
+                                          C.POINTER(_Failure)]),
     "f2v_get_rows": (_i32, [_vp, _u32p, C.c_uint32, _f32p]),
     "f2v_set_rows": (_i32, [_vp, _u32p, C.c_uint32, _f32p]),
 }
@@ -552,10 +556,28 @@ class Device:
             counters.repulsive_evals += ctr.repulsive_evals
         return loss.value if monitor else None
 
+    # ------------------------------ per-step all-gather baseline (NCCL)
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(_lib.f2v_nccl_unique_id(buf))
+        return buf.raw
+
+    def nccl_init(self, unique_id: bytes, rank: int, world: int):
+        self._ck(_lib.f2v_nccl_init(self._h, unique_id, rank, world))
+
+    def train_epochs_allgather(self, cfg: TrainConfig, first_epoch: int = 0,
+                               run_epochs: int = 0, counters: Optional[TrainCounters] = None,
+                               failure: Optional[dict] = None) -> list:
+        """The G-shard epochs with a per-step ncclAllGather of the updated rows
+        (f2v_train_epochs_allgather) -- the baseline of the fused NVLink path."""
+        return self.train_epochs(cfg, first_epoch, run_epochs, counters=counters,
+                                 failure=failure, _fn=_lib.f2v_train_epochs_allgather)
+
     def train_epochs(self, cfg: TrainConfig, first_epoch: int = 0, run_epochs: int = 0,
                      init: bool = False, counters: Optional[TrainCounters] = None,
                      failure: Optional[dict] = None, first_batch: int = 0,
-                     run_batches: int = 0) -> list:
+                     run_batches: int = 0, _fn=None) -> list:
         """Device-resident epochs [first_epoch, first_epoch + run_epochs) of
         train()'s cfg.epochs-long schedule (run_epochs 0: through the end).
         run_batches > 0 (with run_epochs == 1): only steps [first_batch,
@@ -568,8 +590,8 @@ class Device:
         losses = np.zeros(max(nep, 1), np.float64)
         ctr = _Counters()
         fail = _Failure()
-        rc = _lib.f2v_train_epochs(self._h, C.byref(c), losses.ctypes.data_as(_vp),
-                                   C.byref(ctr), C.byref(fail))
+        rc = (_fn or _lib.f2v_train_epochs)(self._h, C.byref(c), losses.ctypes.data_as(_vp),
+                                            C.byref(ctr), C.byref(fail))
         if rc == 4 and failure is not None:
             failure.update(epoch=fail.epoch, batch=fail.batch, vertex=fail.vertex)
         self._ck(rc)

@@ -130,10 +130,12 @@ static uint64_t degree_sum(const Ctx& c, const uint32_t* ids, uint32_t b) {
 // grad_minibatch + batch_loss + apply_update (220-236).
 static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_out,
                               f2v_counters* counters, f2v_failure* failure);
+static void train_allgather_impl(Ctx& c, const f2v_train_config& cfg, double* loss_out,
+                                 f2v_counters* counters, f2v_failure* failure);
 
 // Timing wrapper: CUDA events on the context stream around the whole call.
 static void train_epochs(Ctx& c, const f2v_train_config& cfg, double* loss_out,
-                         f2v_counters* counters, f2v_failure* failure) {
+                         f2v_counters* counters, f2v_failure* failure, bool allgather = false) {
   if (!c.ev_begin) {
     F2V_CUDA(cudaEventCreate(&c.ev_begin));
     F2V_CUDA(cudaEventCreate(&c.ev_end));
@@ -141,7 +143,8 @@ static void train_epochs(Ctx& c, const f2v_train_config& cfg, double* loss_out,
   for (double& t : c.timing) t = 0.0;
   const auto t0 = std::chrono::steady_clock::now();
   F2V_CUDA(cudaEventRecord(c.ev_begin, c.stream));
-  train_epochs_impl(c, cfg, loss_out, counters, failure);
+  if (allgather) train_allgather_impl(c, cfg, loss_out, counters, failure);
+  else train_epochs_impl(c, cfg, loss_out, counters, failure);
   F2V_CUDA(cudaEventRecord(c.ev_end, c.stream));
   F2V_CUDA(cudaEventSynchronize(c.ev_end));
   float ms = 0.f;
@@ -257,6 +260,74 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
   }
 }
 
+// The same epochs with the per-step all-gather baseline (f2v_nccl.cu): each
+// process runs its shard's batch of every step and exchanges the updated rows
+// with ncclAllGather; same semantics and results as the fused path.
+static void train_allgather_impl(Ctx& c, const f2v_train_config& cfg, double* loss_out,
+                                 f2v_counters* counters, f2v_failure* failure) {
+  need_graph(c);
+  if (!c.nccl_comm) fail(F2V_EUSAGE, "f2v_nccl_init first");
+  if (c.shard_ready) fail(F2V_EUSAGE, "an IPC-attached context runs the fused path");
+  if (cfg.dim < 1) fail(F2V_EUSAGE, "dim must be >= 1");
+  if (cfg.batch < 1) fail(F2V_EUSAGE, "batch must be >= 1");
+  if (cfg.negatives < 1) fail(F2V_EUSAGE, "negatives must be >= 1");
+  if (!(cfg.lr > 0)) fail(F2V_EUSAGE, "lr must be > 0");
+  if (cfg.epochs < 1) fail(F2V_EUSAGE, "epochs must be >= 1");
+  if (cfg.first_epoch >= cfg.epochs) fail(F2V_EUSAGE, "first_epoch must be < epochs");
+  if (cfg.walk_length || cfg.run_batches)
+    fail(F2V_EUNSUPPORTED, "the all-gather baseline runs one-hop whole epochs");
+  validate_model(cfg.model);
+  if (cfg.monitor_loss && cfg.model.kind != F2V_SIGMOID && cfg.model.kind != F2V_TDIST)
+    fail(F2V_EUNSUPPORTED, "loss monitoring requires the sigmoid or tdist model");
+  if (cfg.sampler != F2V_SAMPLER_SPLITMIX && cfg.sampler != F2V_SAMPLER_PHILOX)
+    fail(F2V_EUSAGE, "unknown sampler");
+  if (cfg.precision != F2V_PRECISION_FAST && cfg.precision != F2V_PRECISION_EXACT)
+    fail(F2V_EUSAGE, "unknown precision");
+  const uint32_t G = c.nccl_world;
+  if (cfg.shards && cfg.shards != G) fail(F2V_EUSAGE, "cfg.shards must equal the NCCL world");
+  if (cfg.init == 1) {
+    c.d = cfg.dim;
+    c.cur = 0;
+    c.z[0].ensure(sizeof(float) * size_t(c.n) * c.d);
+    k_uniform_embedding(c, cfg.seed, 0.f, 0.f, 1);
+  } else {
+    need_embedding(c);
+    if (c.d != cfg.dim) fail(F2V_ERANGE, "embedding dim does not match cfg.dim");
+  }
+  const uint32_t end_epoch =
+      cfg.run_epochs ? std::min(cfg.epochs, cfg.first_epoch + cfg.run_epochs) : cfg.epochs;
+  const uint32_t s = cfg.negatives;
+  const ForceParams fp = make_params(cfg.model);
+  k_shard_layout(c, cfg.batch, G, s);
+  k_set_context(c, 0);
+  uint64_t attr = 0, rep = 0;
+  for (uint32_t e = cfg.first_epoch; e < end_epoch; ++e) {
+    float eta = cfg.lr;
+    if (cfg.lr_decay) eta = cfg.lr * (1.0f - float(e) / float(cfg.epochs));
+    k_epoch_perm(c, e, cfg.seed);  // every shard's partition_epoch, combined order
+    k_epoch_negatives(c, s, e, cfg.seed, cfg.sampler);
+    const AgResult r = k_allgather_epoch(c, s, eta, fp, cfg.monitor_loss != 0,
+                                         cfg.precision == F2V_PRECISION_FAST);
+    if (r.failed) {  // no rank applied the failing step (trainer.cpp:149-152)
+      if (failure) {
+        failure->epoch = e;
+        failure->batch = r.step;
+        failure->vertex = r.vertex;
+      }
+      fail(F2V_ENUMERICAL, "non-finite gradient for vertex " + std::to_string(r.vertex) +
+                               " (epoch " + std::to_string(e) + ", batch " +
+                               std::to_string(r.step) + ")");
+    }
+    if (cfg.monitor_loss && loss_out) loss_out[e - cfg.first_epoch] = r.loss;
+    attr += c.nnz;
+    rep += uint64_t(c.n) * s;
+  }
+  if (counters) {
+    counters->attractive_evals += attr;
+    counters->repulsive_evals += rep;
+  }
+}
+
 }  // namespace f2v
 
 using namespace f2v;
@@ -309,6 +380,11 @@ void f2v_destroy(f2v_ctx* h) {
       if (c.peer_base[g][i]) cudaIpcCloseMemHandle(c.peer_base[g][i]);
   c.ctl.release();
   for (DeviceBuf& r : c.rep) r.release();
+  for (DeviceBuf* b : {&c.ag_send, &c.ag_recv, &c.ag_state}) b->release();
+  try {
+    k_nccl_destroy(c);
+  } catch (...) {
+  }
   for (cudaEvent_t e : c.ev_kernel) cudaEventDestroy(e);
   if (c.ev_begin) cudaEventDestroy(c.ev_begin);
   if (c.ev_end) cudaEventDestroy(c.ev_end);
@@ -553,6 +629,25 @@ int32_t f2v_train(int32_t device, uint32_t n, const uint64_t* row_offsets,
   if (rc != F2V_OK) g_global_err = h->c.err;
   f2v_destroy(h);
   return rc;
+}
+
+int32_t f2v_nccl_unique_id(uint8_t* out) {
+  return guard(nullptr, [&] { nccl_unique_id(out); });
+}
+
+int32_t f2v_nccl_init(f2v_ctx* h, const uint8_t* unique_id, uint32_t rank, uint32_t world) {
+  return guard(&h->c, [&] {
+    F2V_CUDA(cudaSetDevice(h->c.device));
+    k_nccl_init(h->c, unique_id, rank, world);
+  });
+}
+
+int32_t f2v_train_epochs_allgather(f2v_ctx* h, const f2v_train_config* cfg, double* loss_out,
+                                   f2v_counters* counters, f2v_failure* failure) {
+  return guard(&h->c, [&] {
+    F2V_CUDA(cudaSetDevice(h->c.device));
+    train_epochs(h->c, *cfg, loss_out, counters, failure, true);
+  });
 }
 
 int32_t f2v_csr_from_edges(const uint32_t* pairs, uint64_t m, uint32_t n, int32_t symmetrize,

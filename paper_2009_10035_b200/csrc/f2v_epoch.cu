@@ -455,6 +455,19 @@ void k_epoch_perm(Ctx& c, uint32_t epoch, uint64_t seed) {
   ++c.launches;
 }
 
+// The negatives of every (step, shard) set of this epoch (after k_epoch_perm),
+// for the per-step all-gather driver (f2v_nccl.cu).
+void k_epoch_negatives(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sampler) {
+  const uint64_t nsets = uint64_t(c.steps) * c.shards;
+  c.negs_all.ensure(sizeof(uint32_t) * std::max<uint64_t>(nsets * s, 1));
+  c.negwin.ensure(sizeof(uint32_t) * std::max<uint64_t>(nsets, 1));
+  negs_kernel<<<uint32_t((nsets + 255) / 256), 256, 0, c.stream>>>(
+      c.negs_all.as<uint32_t>(), c.negwin.as<uint32_t>(), c.state.as<uint32_t>(), make_geo(c),
+      nsets, s, seed, epoch, sampler, c.tune.window, 0, nullptr, c.poff.as<uint32_t>());
+  F2V_LAUNCHED(c.stream, "negs_kernel");
+  ++c.launches;
+}
+
 // Per-epoch preparation after k_epoch_perm: the negatives of every (step,
 // shard) set + window flags, the window pre-scan, the two ordered item lists
 // (only this process's rows when the shards run on several GPUs).

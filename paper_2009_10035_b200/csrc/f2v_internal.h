@@ -115,6 +115,10 @@ struct Ctx {
   std::vector<uint32_t> sh_lo, sh_bs, sh_nb;  // per shard: first row, batch, batches
   // multi-process: IPC-shared control block + the peers' replicas (f2v_shard.cu)
   DeviceBuf ctl;
+  // per-step all-gather baseline (f2v_nccl.cu): NCCL communicator + packs
+  void* nccl_comm = nullptr;
+  uint32_t nccl_rank = 0, nccl_world = 1;
+  DeviceBuf ag_send, ag_recv, ag_state;
   DeviceBuf rep[7];  // emulated peer replicas of Znew (F2V_EMULATE_REPLICAS, tests)
   bool shard_ready = false;
   float* peer_z[8][2] = {};
@@ -172,5 +176,18 @@ size_t shard_ctl_bytes();
 void k_rows(Ctx& c, uint32_t b, float* rows_dev, bool to_z);  // rows <-> Z[c.ids]
 
 ForceParams make_params(const f2v_force_model& m);
+
+// per-step all-gather baseline (f2v_nccl.cu)
+struct AgResult {
+  bool failed;
+  uint32_t step, rank, index, vertex;
+  double loss;
+};
+void nccl_unique_id(uint8_t* out128);
+void k_nccl_init(Ctx& c, const uint8_t* id128, uint32_t rank, uint32_t world);
+void k_nccl_destroy(Ctx& c);
+void k_epoch_negatives(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sampler);
+AgResult k_allgather_epoch(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bool monitor,
+                           bool fast);
 
 }  // namespace f2v

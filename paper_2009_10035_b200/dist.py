@@ -40,8 +40,8 @@ import numpy as np
 from . import (CsrGraph, Device, NumericalError, TrainConfig, TrainCounters, UsageError,
                negatives, partition_shard, shard_layout)
 
-__all__ = ["env_rank", "ShardedDevice", "StepBackend", "DeviceBackend", "train_allgather",
-           "shard_steps"]
+__all__ = ["env_rank", "ShardedDevice", "AllgatherDevice", "StepBackend", "DeviceBackend",
+           "train_allgather", "shard_steps"]
 
 
 def env_rank() -> Tuple[int, int, int]:
@@ -119,6 +119,54 @@ class ShardedDevice:
     @property
     def kernel_launches(self) -> int:
         return self.dev.kernel_launches
+
+
+# ------------------------------------ per-step ncclAllGather (in the library)
+class AllgatherDevice:
+    """One rank of the per-step all-gather baseline run inside the library
+    (f2v_train_epochs_allgather): every step's updated rows are exchanged
+    with ncclAllGather on the context stream, no host staging.  Rank 0's NCCL
+    unique id is broadcast through torch.distributed (any backend)."""
+
+    def __init__(self, rank: Optional[int] = None, world: Optional[int] = None,
+                 device: Optional[int] = None, group=None):
+        r, w, local = env_rank()
+        self.rank = r if rank is None else rank
+        self.world = w if world is None else world
+        self.group = group
+        self.dev = Device(local if device is None else device)
+
+    def close(self):
+        self.dev.close()
+
+    def setup(self, g: CsrGraph, z0: Optional[np.ndarray] = None, dim: int = 128,
+              seed: int = 1, lo: float = -1.0, hi: float = 1.0):
+        self.dev.upload_graph(g)
+        if z0 is not None:
+            self.dev.set_embedding(z0)
+        else:
+            self.dev.uniform_embedding(g.num_vertices(), dim, seed, lo, hi)
+        uid = Device.nccl_unique_id() if self.rank == 0 else None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            box = [uid]
+            dist.broadcast_object_list(box, src=0, group=self.group)
+            uid = box[0]
+        self.dev.nccl_init(uid, self.rank, self.world)
+
+    def train_epochs(self, cfg: TrainConfig, first_epoch: int = 0, run_epochs: int = 0,
+                     counters: Optional[TrainCounters] = None,
+                     failure: Optional[dict] = None) -> list:
+        c = dataclasses.replace(cfg, shards=self.world)
+        return self.dev.train_epochs_allgather(c, first_epoch, run_epochs, counters=counters,
+                                               failure=failure)
+
+    def get_embedding(self) -> np.ndarray:
+        return self.dev.get_embedding()
+
+    def last_timing(self) -> dict:
+        return self.dev.last_timing()
 
 
 # ---------------------------------------------- per-step all-gather baseline

@@ -221,3 +221,67 @@ def test_emulated_replicas_match_oracle(f2v, orc, dev, precision, G, kind, d):
     np.testing.assert_allclose(outs[1][0], lr_, rtol=1e-3)
     rel = np.linalg.norm(outs[1][1].astype(np.float64) - zr) / np.linalg.norm(zr)
     assert rel < 1e-4, rel
+
+
+@pytest.mark.parametrize("precision,sampler,kind", [("exact", "splitmix", "sigmoid"),
+                                                    ("exact", "philox", "tdist"),
+                                                    ("fast", "philox", "sigmoid"),
+                                                    ("fast", "philox", "tdist")])
+def test_nccl_allgather_library_world1(f2v, orc, precision, sampler, kind):
+    """The in-library per-step ncclAllGather baseline (f2v_train_epochs_allgather,
+    world-1 NCCL communicator): device-resident grad -> pack -> all-gather ->
+    vote -> scatter per step, no host staging.  Against the oracle's train();
+    EXACT with the reference's own streams is bit-identical in practice."""
+    from paper_2009_10035_b200.dist import AllgatherDevice
+
+    g = _graph(f2v, orc, 1800, 4)
+    n = g.num_vertices()
+    z0 = np.zeros((n, 128), np.float32)
+    orc.oracle().orc_random_embedding(n, 128, 2, z0)
+    cfg = f2v.TrainConfig(dim=128, batch=100, negatives=5, lr=0.02, epochs=2,
+                          model=kind_model(f2v, kind), seed=4, monitor_loss=True,
+                          sampler=sampler, precision=precision)
+    ag = AllgatherDevice(rank=0, world=1, device=0)
+    try:
+        ag.setup(g, z0)
+        ctr = f2v.TrainCounters()
+        losses = ag.train_epochs(cfg, counters=ctr)
+        z = ag.get_embedding()
+    finally:
+        ag.close()
+    rc, zr, lr_, cr, _ = orc.orc_train(g.row_offsets, g.col_indices, z0, 100, 5, 0.02, 2, kind,
+                                       4, sampler=sampler, threads=8)
+    assert rc == 0
+    _, _, same = z_parity(z, zr)
+    if precision == "exact":
+        assert same >= 0.9999, same
+    np.testing.assert_allclose(losses, lr_, rtol=LOSS_RTOL[precision])
+    assert [ctr.attractive_evals, ctr.repulsive_evals] == [int(cr[0]), int(cr[1])]
+
+
+def test_nccl_allgather_library_failure(f2v, orc):
+    """A non-finite gradient stops every rank at the oracle's (epoch, batch,
+    vertex), Z left at the last complete step (trainer.cpp:149-152)."""
+    from paper_2009_10035_b200.dist import AllgatherDevice
+
+    rp, col = orc.orc_sbm_graph(300, 3, 0.1, 0.01, 5)
+    g = f2v.CsrGraph(rp, col)
+    z0 = np.zeros((300, 128), np.float32)
+    orc.oracle().orc_random_embedding(300, 128, 2, z0)
+    z0[123] = 3e37  # FR attraction r^2 overflows fp32 for 123's neighbours
+    cfg = f2v.TrainConfig(dim=128, batch=16, negatives=3, lr=0.02, epochs=2,
+                          model=kind_model(f2v, "fr"), seed=6, precision="exact")
+    ag = AllgatherDevice(rank=0, world=1, device=0)
+    fail = {}
+    try:
+        ag.setup(g, z0)
+        with pytest.raises(f2v.NumericalError, match=r"non-finite gradient for vertex \d+ "
+                                                     r"\(epoch 0, batch \d+\)"):
+            ag.train_epochs(cfg, failure=fail)
+        z = ag.get_embedding()
+    finally:
+        ag.close()
+    rc, zr, _, _, finfo = orc.orc_train(rp, col, z0, 16, 3, 0.02, 2, "fr", 6, monitor=False)
+    assert rc == 4
+    assert (fail["epoch"], fail["batch"], fail["vertex"]) == tuple(int(x) for x in finfo)
+    z_parity(z, zr)
