@@ -437,6 +437,37 @@ def bench_b200(args):
                 "clocks": f_clk,
                 "note": "precision='fast': fp32 dot/distance and force term, fp32 8-pair "
                         "block sums, fp64 per-vertex accumulation; not the headline"}
+    # ------------------------------------- per-step all-gather baseline
+    # the same epochs run step by step (grad -> ncclAllGather of the updated
+    # rows -> scatter), the reference's synchronisation granularity: what the
+    # fused dataflow kernel is measured against (SURVEY.md 8(e) ladder step 1)
+    per_step = None
+    if not args.no_per_step:
+        try:
+            from paper_2009_10035_b200.dist import AllgatherDevice
+            ag = AllgatherDevice(rank, world, local)
+            ag.setup(g, dim=d, seed=1)
+            cfg_ag = dataclasses.replace(cfg, shards=world)
+            ag.train_epochs(cfg_ag, 0, 1)  # warm-up epoch
+            ks = max(1, min(args.steps, 2))
+            ag.train_epochs(cfg_ag, 1, ks)
+            t_ag = ag.last_timing()["device_ms"]
+            if world > 1:
+                import torch
+                import torch.distributed as dist
+                tt = torch.tensor([t_ag], device=f"cuda:{local}")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t_ag = float(tt.item())
+            ag.close()
+            per_step = {"value": pairs * ks / (t_ag / 1e3), "unit": "updates/s",
+                        "ms_per_step": t_ag / ks, "epochs": ks,
+                        "exchange": f"ncclAllGather of every step's updated rows, world {world}",
+                        "dtype": PRECISION_DTYPE[args.precision],
+                        "note": "f2v_train_epochs_allgather: per step one grad kernel "
+                                "(one warp per batch row), the all-gather, a vote and a "
+                                "scatter kernel; same results as the fused epoch kernel"}
+        except Exception as ex:  # reported, not hidden
+            per_step = {"value": None, "error": str(ex)}
     # ------------------------------------------------------------ e2e
     import torch
     h_row = torch.from_numpy(g.row_offsets).pin_memory().numpy()
@@ -512,6 +543,8 @@ def bench_b200(args):
     }
     if fast is not None:
         out["fast"] = fast
+    if per_step is not None:
+        out["per_step_baseline"] = per_step
     if world == 1 and not args.no_cpu_baseline:
         try:
             import pyoracle as P
@@ -538,6 +571,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fast", action="store_true", help="skip the precision='fast' run")
+    ap.add_argument("--no-per-step", action="store_true",
+                    help="skip the per-step ncclAllGather baseline")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         log("note: warm-up raised to the contract minimum of 3")

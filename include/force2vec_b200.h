@@ -132,6 +132,17 @@ int32_t f2v_last_timing(const f2v_ctx* ctx, double* out4);
 int32_t f2v_upload_graph(f2v_ctx* ctx, uint32_t n, const uint64_t* row_offsets,
                          const uint32_t* col_indices, uint64_t nnz);
 /* EmbeddingMatrix (trainer.hpp:33-57): row-major f32[n*d] */
+/* CsrGraph::from_edges (csr_graph.cpp:57-97) ON THE DEVICE into the context's
+ * graph: self-loops dropped (counted), reversed arcs added when symmetrize,
+ * sorted, deduplicated -- the same CSR, byte for byte, as f2v_csr_from_edges
+ * (F2V_ERANGE for an endpoint >= n).  Replaces f2v_upload_graph for graphs
+ * whose host build is the bottleneck (C5: 2.1B arcs). */
+int32_t f2v_build_graph(f2v_ctx* ctx, const uint32_t* pairs, uint64_t m, uint32_t n,
+                        int32_t symmetrize, uint64_t* nnz_out, uint64_t* duplicates_dropped,
+                        uint64_t* self_loops_dropped);
+/* the context's CSR (e.g. built by f2v_build_graph) copied out:
+ * row_offsets_out[n + 1], col_out[nnz] */
+int32_t f2v_get_graph(f2v_ctx* ctx, uint64_t* row_offsets_out, uint32_t* col_out);
 int32_t f2v_set_embedding(f2v_ctx* ctx, const float* z, uint32_t n, uint32_t d);
 int32_t f2v_get_embedding(f2v_ctx* ctx, float* z);
 /* init_embedding (trainer.cpp:62-72): U(-0.5/d, 0.5/d) keyed (seed,{0x11}) */

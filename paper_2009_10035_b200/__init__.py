@@ -113,6 +113,9 @@ SYMBOLS = {
     "f2v_kernel_launches": (C.c_uint64, [_vp, _i32]),
     "f2v_last_timing": (_i32, [_vp, _f64p]),
     "f2v_upload_graph": (_i32, [_vp, C.c_uint32, _u64p, _u32p, C.c_uint64]),
+    "f2v_build_graph": (_i32, [_vp, _u32p, C.c_uint64, C.c_uint32, _i32, C.POINTER(C.c_uint64),
+                               C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "f2v_get_graph": (_i32, [_vp, _u64p, _u32p]),
     "f2v_set_embedding": (_i32, [_vp, _f32p, C.c_uint32, C.c_uint32]),
     "f2v_get_embedding": (_i32, [_vp, _f32p]),
     "f2v_init_embedding": (_i32, [_vp, C.c_uint32, C.c_uint32, C.c_uint64]),
@@ -486,6 +489,28 @@ class Device:
                                        g.col_indices if g.num_edges() else np.zeros(1, np.uint32),
                                        g.num_edges()))
         self.n = g.num_vertices()
+        self._nnz = g.num_edges()
+
+    def build_graph(self, edges, n: int, symmetrize: bool = True):
+        """CsrGraph::from_edges (csr_graph.cpp:57-97) on the device, into this
+        context (f2v_build_graph).  Returns (nnz, duplicates_dropped,
+        self_loops_dropped)."""
+        pairs = np.ascontiguousarray(edges, np.uint32).reshape(-1)
+        m = len(pairs) // 2
+        nnz, dups, loops = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._ck(_lib.f2v_build_graph(self._h, pairs if m else np.zeros(2, np.uint32), m, n,
+                                      int(symmetrize), C.byref(nnz), C.byref(dups),
+                                      C.byref(loops)))
+        self.n = n
+        self._nnz = nnz.value
+        return nnz.value, dups.value, loops.value
+
+    def get_graph(self) -> "CsrGraph":
+        """The context's CSR copied out (f2v_get_graph)."""
+        rowptr = np.zeros(self.n + 1, np.uint64)
+        col = np.zeros(max(self._nnz, 1), np.uint32)
+        self._ck(_lib.f2v_get_graph(self._h, rowptr, col))
+        return CsrGraph(rowptr, col[: self._nnz])
 
     def set_embedding(self, z: np.ndarray):
         z = np.ascontiguousarray(z, np.float32)

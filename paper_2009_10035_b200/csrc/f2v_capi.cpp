@@ -447,6 +447,48 @@ int32_t f2v_upload_graph(f2v_ctx* h, uint32_t n, const uint64_t* row_offsets,
   });
 }
 
+int32_t f2v_build_graph(f2v_ctx* h, const uint32_t* pairs, uint64_t m, uint32_t n,
+                        int32_t symmetrize, uint64_t* nnz_out, uint64_t* dups_out,
+                        uint64_t* loops_out) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    F2V_CUDA(cudaSetDevice(c.device));
+    if (c.walk_k) {  // drop a walk context of the previous graph
+      c.grow.release();
+      c.gcol.release();
+      c.h_growptr.clear();
+      c.walk_k = 0;
+    }
+    uint64_t nnz = 0;
+    device_csr_from_edges(c.stream, c.num_sms, pairs, m, n, symmetrize != 0, c.rowptr, c.col,
+                          &nnz, dups_out, loops_out);
+    c.n = n;
+    c.nnz = nnz;
+    ++c.graph_gen;
+    c.h_rowptr.resize(size_t(n) + 1);
+    F2V_CUDA(cudaMemcpyAsync(c.h_rowptr.data(), c.rowptr.p, sizeof(uint64_t) * (size_t(n) + 1),
+                             cudaMemcpyDeviceToHost, c.stream));
+    F2V_CUDA(cudaStreamSynchronize(c.stream));
+    if (nnz_out) *nnz_out = nnz;
+    k_prepare_graph(c);
+  });
+}
+
+int32_t f2v_get_graph(f2v_ctx* h, uint64_t* row_offsets_out, uint32_t* col_out) {
+  return guard(&h->c, [&] {
+    Ctx& c = h->c;
+    need_graph(c);
+    if (c.walk_k) fail(F2V_EUSAGE, "a walk context is active");
+    F2V_CUDA(cudaSetDevice(c.device));
+    F2V_CUDA(cudaMemcpyAsync(row_offsets_out, c.rowptr.p, sizeof(uint64_t) * (size_t(c.n) + 1),
+                             cudaMemcpyDeviceToHost, c.stream));
+    if (c.nnz)
+      F2V_CUDA(cudaMemcpyAsync(col_out, c.col.p, sizeof(uint32_t) * c.nnz, cudaMemcpyDeviceToHost,
+                               c.stream));
+    F2V_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
 int32_t f2v_set_embedding(f2v_ctx* h, const float* z, uint32_t n, uint32_t d) {
   return guard(&h->c, [&] {
     Ctx& c = h->c;

@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) epoch_kernel(EpochArgs a) {
   const int w = threadIdx.x >> 5;
   uint32_t* qbuf = qs[w];
   uint32_t* rbuf = rs[w];
+  if (uses_ring<K, VEC, FAST>()) ring_init(lane);
   const bool lrole = w >= kWarps - int(a.lwarps);
   uint32_t* counter = a.next + (lrole ? 1 : 0);
   const uint32_t total = lrole ? *a.n_litems : *a.n_eitems_dev;
@@ -548,28 +549,33 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) epoch_kernel(EpochArgs a) {
 template <int KIND, int K, bool VEC, bool MON, bool FAST, int MINB>
 void launch_one(Ctx& c, const EpochArgs& a) {
   auto kern = epoch_kernel<KIND, K, VEC, MON, FAST, MINB>;
+  const size_t dsmem = uses_ring<K, VEC, FAST>() ? size_t(kWarps) * kRingWarpBytes : 0;
+  if (dsmem) F2V_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(dsmem)));
   if (c.dry_launch) {  // load the function only (CUDA lazy loading) -- no launch
     cudaFuncAttributes fa;
     F2V_CUDA(cudaFuncGetAttributes(&fa, kern));
     return;
   }
   int per_sm = 0;
-  F2V_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, 0));
+  F2V_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, dsmem));
   if (c.tune.ctas && int(c.tune.ctas) < per_sm) per_sm = int(c.tune.ctas);
   if (per_sm < 1) per_sm = 1;
   uint32_t blocks = uint32_t(per_sm) * uint32_t(c.num_sms);
   const uint64_t ew = kWarps - a.lwarps;
   const uint32_t need = uint32_t(std::max<uint64_t>((a.n_eitems + ew - 1) / ew, 1));
   blocks = std::max(1u, std::min(blocks, need));
-  kern<<<blocks, kWarps * 32, 0, c.stream>>>(a);
+  kern<<<blocks, kWarps * 32, dsmem, c.stream>>>(a);
   F2V_LAUNCHED(c.stream, "kern");
   ++c.launches;
 }
 
 #ifndef F2V_EXACT_MINB
-// EXACT d = 128 register budget (resident 8-warp CTAs per SM): 3 (80
-// registers, 24 warps/SM) measured 57.7 ms on C3 against 65.1 ms at 2 (128)
-#define F2V_EXACT_MINB 3
+// EXACT d = 128 register budget (resident 8-warp CTAs per SM).  Register
+// gathers: 3 (80 registers, 24 warps/SM) measured 57.7 ms on C3 against 65.1
+// ms at 2 (128); with the TMA row ring (F2V_ROW_TMA_EXACT) 2 is better: 62.6
+// ms against 75.6 ms at 3 (the ring's shared memory halves the resident L1)
+#define F2V_EXACT_MINB (F2V_ROW_TMA_EXACT ? 2 : 3)
 #endif
 
 template <int KIND, int K, bool VEC, bool FAST>

@@ -177,6 +177,11 @@ void k_rows(Ctx& c, uint32_t b, float* rows_dev, bool to_z);  // rows <-> Z[c.id
 
 ForceParams make_params(const f2v_force_model& m);
 
+// CsrGraph::from_edges on the device (f2v_csr.cu)
+void device_csr_from_edges(cudaStream_t st, int num_sms, const uint32_t* pairs_host, uint64_t m,
+                           uint32_t n, bool symmetrize, DeviceBuf& rowptr_dev, DeviceBuf& col_dev,
+                           uint64_t* nnz_out, uint64_t* dups_out, uint64_t* loops_out);
+
 // per-step all-gather baseline (f2v_nccl.cu)
 struct AgResult {
   bool failed;

@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(256) ag_step_kernel(AgArgs a) {
   // hdr->fail was reset to ~0 by the previous step's vote (or the epoch start)
   if (blockIdx.x == 0 && threadIdx.x == 0) hdr->count = cnt;
   const int lane = threadIdx.x & 31;
+  if (uses_ring<K, VEC, FAST>()) ring_init(lane);
   const uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (i >= cnt) return;
   const uint32_t u = a.perm[a.p0 + i];
@@ -203,8 +204,15 @@ __global__ void ag_scatter_kernel(AgArgs a) {
 template <int KIND, int K, bool VEC, bool FAST>
 void launch_ag_step(const AgArgs& a, bool mon, cudaStream_t st) {
   const uint32_t blocks = std::max(1u, (a.cnt * 32 + 255) / 256);
-  if (mon) ag_step_kernel<KIND, K, VEC, true, FAST><<<blocks, 256, 0, st>>>(a);
-  else ag_step_kernel<KIND, K, VEC, false, FAST><<<blocks, 256, 0, st>>>(a);
+  const size_t dsmem = uses_ring<K, VEC, FAST>() ? 8 * kRingWarpBytes : 0;
+  auto k1 = ag_step_kernel<KIND, K, VEC, true, FAST>;
+  auto k0 = ag_step_kernel<KIND, K, VEC, false, FAST>;
+  if (dsmem) {
+    F2V_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsmem)));
+    F2V_CUDA(cudaFuncSetAttribute(k0, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dsmem)));
+  }
+  if (mon) k1<<<blocks, 256, dsmem, st>>>(a);
+  else k0<<<blocks, 256, dsmem, st>>>(a);
 }
 
 // d = 128 (the bench row width) per force kind, FAST or EXACT; any other d

@@ -160,6 +160,94 @@ struct Lay {
   }
 };
 
+// ------------------------------------------------ TMA row ring (F2V_ROW_TMA)
+// Each warp owns kRingStages x 8 row slots of 512 bytes in dynamic shared
+// memory plus one mbarrier per stage.  A block of up to 8 neighbour rows is
+// fetched by bulk async copies (cp.async.bulk global -> shared, completion
+// counted in bytes on the stage's mbarrier; one row per lane 0..7), so the
+// next block's gathers are in flight -- without registers -- while this
+// block's pair math runs.  The copies read L2 like ld.cg; Znew rows still go
+// through the sentinel check (and the poll on direct loads).
+// Measured and not enabled by default (same box, A/B): FAST C3 30.6 -> 30.4 ms,
+// FAST C2 8.35 -> 9.03 ms (the ring's loads bypass L1, where R-MAT's hub rows
+// hit), EXACT C3 61.4 -> 62.6 ms at 2 CTAs/SM and 75.6 ms at 3 (the fp64 pair
+// math, not the gathers, bounds EXACT; the 128 KB+ carve-out costs L1).
+// Compile with -DF2V_ROW_TMA_EXACT=1 / -DF2V_ROW_TMA_FAST=1 to use it.
+#ifndef F2V_ROW_TMA_EXACT
+#define F2V_ROW_TMA_EXACT 0
+#endif
+#ifndef F2V_ROW_TMA_FAST
+#define F2V_ROW_TMA_FAST 0
+#endif
+constexpr int kRingStages = 2;
+constexpr uint32_t kRowBytes = 512;  // d = 128 rows (the ring serves the VEC K = 4 layouts)
+constexpr uint32_t kRingWarpBytes = 128 + kRingStages * 8 * kRowBytes;  // barriers + slots
+
+// the row layouts that stream through the ring (kernels launch with its
+// dynamic shared memory and initialise it)
+template <int K, bool VEC, bool FAST>
+__host__ __device__ constexpr bool uses_ring() {
+  return K == 4 && VEC && (FAST ? F2V_ROW_TMA_FAST != 0 : F2V_ROW_TMA_EXACT != 0);
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return uint32_t(__cvta_generic_to_shared(p));
+}
+extern __shared__ __align__(128) uint8_t f2v_dsmem[];
+// this warp's ring: [0, 8 S) mbarriers, [64] phase bits, slots from 128
+__device__ __forceinline__ uint8_t* ring_base() {
+  return f2v_dsmem + (threadIdx.x >> 5) * kRingWarpBytes;
+}
+__device__ __forceinline__ void ring_init(int lane) {
+  uint8_t* b = ring_base();
+  if (lane == 0) {
+    for (int s = 0; s < kRingStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(b + 8 * s)));
+    *reinterpret_cast<uint32_t*>(b + 64) = 0u;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
+// fetch rows (packed ids of rows k0..k0+7 of the call; nr <= 8 valid) into stage st
+__device__ __forceinline__ void ring_issue(int st, uint32_t packed, int k0, int nr, int lane,
+                                           const float* zold, const float* znew) {
+  uint8_t* b = ring_base();
+  const uint32_t bar = smem_addr(b + 8 * st);
+  const uint32_t pk = __shfl_sync(kFull, packed, (k0 + (lane & 7)) & 31);
+  if (lane == 0)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(uint32_t(nr) * kRowBytes)
+                 : "memory");
+  if (lane < nr) {
+    const float* src = ((pk & kNewBit) ? znew : zold) + size_t(pk & ~kNewBit) * (kRowBytes / 4);
+    const uint32_t dst = smem_addr(b + 128 + (st * 8 + lane) * kRowBytes);
+    // the slot's previous rows were read through the generic proxy
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst), "l"(src), "r"(kRowBytes), "r"(bar)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void ring_wait(int st, uint32_t& ph) {
+  const uint32_t bar = smem_addr(ring_base() + 8 * st);
+  const uint32_t par = (ph >> st) & 1u;
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(par)
+      : "memory");
+  ph ^= 1u << st;
+}
+// row i of stage st into registers (lane holds columns 4 lane .. 4 lane + 3)
+__device__ __forceinline__ void ring_read(int st, int i, int lane, float (&v)[4]) {
+  const float4 t =
+      *reinterpret_cast<const float4*>(ring_base() + 128 + (st * 8 + i) * kRowBytes + 16 * lane);
+  v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+}
+
 // ------------------------------------------------------- per-pair terms
 // Scalar part of one pair: out_j = coef * o_j              (sigmoid)
 //                          out_j = coef * (u_j - o_j) * inv (distance kinds)
@@ -522,6 +610,44 @@ __device__ __forceinline__ void rows_fast(const ForceParams& fp, uint32_t packed
   using L = Lay<K, true>;
   constexpr int NB = F2V_FAST_INFLIGHT;
   d = 32 * K;  // VEC layout: a compile-time row stride
+#if F2V_ROW_TMA_FAST
+  if constexpr (K == 4) {
+    const int nblk = (cnt + 7) / 8;
+    uint32_t* phw = reinterpret_cast<uint32_t*>(ring_base() + 64);
+    uint32_t ph = *phw;
+    for (int b = 0; b < nblk && b < kRingStages; ++b)
+      ring_issue(b, packed, 8 * b, min(8, cnt - 8 * b), lane, zold, znew);
+    for (int b = 0; b < nblk; ++b) {
+      const int st = b % kRingStages, k0 = 8 * b;
+      ring_wait(st, ph);
+      float w[8][K];
+      uint32_t pks[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        pks[i] = __shfl_sync(kFull, packed, (k0 + i) & 31);
+        if (k0 + i < cnt) ring_read(st, i, lane, w[i]);
+        else w[i][0] = w[i][1] = w[i][2] = w[i][3] = 0.0f;
+      }
+      __syncwarp();  // every lane has its rows: the stage takes the block after next
+      if (b + kRingStages < nblk)
+        ring_issue(st, packed, k0 + 8 * kRingStages, min(8, cnt - k0 - 8 * kRingStages), lane,
+                   zold, znew);
+      bool pend = false;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (k0 + i < cnt && (pks[i] & kNewBit)) pend |= has_sentinel<K, 2>(w[i]);
+      if (__any_sync(kFull, pend)) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (k0 + i < cnt && (pks[i] & kNewBit))
+            L::poll(znew + size_t(pks[i] & ~kNewBit) * d, lane, d, w[i], fp.stall);
+      }
+      fast_block<KIND, K, MON, ATT>(fp, k0, cnt, lane, zu, w, acc, lsum);
+    }
+    *phw = ph;
+    return;
+  }
+#endif
   for (int k0 = 0; k0 < cnt; k0 += NB) {
     float w[NB / 8][8][K];
     uint32_t pks[NB];
@@ -711,6 +837,37 @@ __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t pack
       }
     }
     };
+#if F2V_ROW_TMA_EXACT
+  if constexpr (K == 4) {  // the next block's rows stream into the shared-memory ring
+    const int nblk = (cnt + 7) / 8;
+    uint32_t* phw = reinterpret_cast<uint32_t*>(ring_base() + 64);
+    uint32_t ph = *phw;
+    for (int b = 0; b < nblk && b < kRingStages; ++b)
+      ring_issue(b, packed, 8 * b, min(8, cnt - 8 * b), lane, zold, znew);
+    for (int b = 0; b < nblk; ++b) {
+      const int st = b % kRingStages, k0 = 8 * b;
+      ring_wait(st, ph);
+      float v[8][K];
+      uint32_t pks[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        pks[i] = __shfl_sync(kFull, packed, (k0 + i) & 31);
+        if (k0 + i < cnt) ring_read(st, i, lane, v[i]);
+        else v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.0f;
+      }
+      __syncwarp();
+      if (b + kRingStages < nblk)
+        ring_issue(st, packed, k0 + 8 * kRingStages, min(8, cnt - k0 - 8 * kRingStages), lane,
+                   zold, znew);
+      compute_block(k0, v, pks);
+    }
+    *phw = ph;
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc_io[k] = acc[k];
+    lsum_io = lsum;
+    return;
+  } else
+#endif
 #if F2V_EXACT_PIPE
   // software pipeline: the next block's gathers are in flight while this
   // block's fp64 math runs (two register blocks, no dynamic indexing)
