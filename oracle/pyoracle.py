@@ -386,7 +386,8 @@ def orc_train(rowptr, col, z0, batch, s, lr, epochs, kind, seed, eps=1e-6, cap=5
 
 
 def ref_train(rg, z0, batch, s, lr, epochs, kind, seed, eps=1e-6, cap=5.0, lr_decay=False,
-              monitor=True, sampler="philox", workers=None, step_cb=None, walk=0):
+              monitor=True, sampler="philox", workers=None, step_cb=None, walk=0,
+              inplace=False):
     """The UNMODIFIED reference train() loop (trainer.cpp:192-251, oracle/_ref)
     on a RefGraph with an injected initial Z; sampler "philox" injects the
     configs' Philox negatives into each Minibatch (the reference's own
@@ -394,7 +395,7 @@ def ref_train(rg, z0, batch, s, lr, epochs, kind, seed, eps=1e-6, cap=5.0, lr_de
     every apply_update.  Returns (rc, Z, epoch_losses, counters, fail_info)."""
     import ctypes as C
     R = reference()
-    z = np.array(z0, np.float32, copy=True, order="C")
+    z = z0 if inplace else np.array(z0, np.float32, copy=True, order="C")
     n, d = z.shape
     b = min(batch, n)
     nb = (n + b - 1) // b

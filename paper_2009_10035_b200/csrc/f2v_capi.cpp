@@ -213,6 +213,15 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
     Ctx& c;
     ~RangeReset() { c.ranged = false; }
   } range_reset{c};
+  // Several epochs run back to back with no host round trip (the outcome of
+  // each stays on the device); single-epoch calls, batch ranges, attached
+  // multi-GPU contexts and the replica emulation keep the per-epoch sync.
+  const uint32_t nep = end_epoch - cfg.first_epoch;
+  const bool async = nep > 1 && !c.ranged && !c.shard_ready &&
+                     std::getenv("F2V_EMULATE_REPLICAS") == nullptr &&
+                     std::getenv("F2V_SYNC_EPOCHS") == nullptr;
+  std::vector<int> znew_of_epoch;
+  if (async) k_async_begin(c, nep);
   uint64_t attr = 0, rep = 0;
   for (uint32_t e = cfg.first_epoch; e < end_epoch; ++e) {
     float eta = cfg.lr;
@@ -221,7 +230,12 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
     k_epoch_perm(c, e, cfg.seed);
     if (c.walk_k) k_epoch_walks(c, e, cfg.seed);  // build_minibatch's walks (sampling.cpp:50-58)
     k_epoch_begin(c, s, e, cfg.seed, cfg.sampler);
-    const EpochResult r = k_epoch_run(c, s, eta, fp, cfg.monitor_loss != 0);
+    const EpochResult r =
+        k_epoch_run(c, s, eta, fp, cfg.monitor_loss != 0, async ? int(e - cfg.first_epoch) : -1);
+    if (async) {
+      znew_of_epoch.push_back(c.cur);
+      continue;
+    }
     if (r.bad_pos != ~0ull) {
       // the step of the failing position (combined step-major order)
       const uint64_t T = c.steps;
@@ -253,6 +267,32 @@ static void train_epochs_impl(Ctx& c, const f2v_train_config& cfg, double* loss_
     }
     attr += c.nnz;            // one-hop: every arc once per epoch (trainer.cpp:154-160)
     rep += uint64_t(n) * s;   // b*s per batch (trainer.cpp:161-162)
+  }
+  if (async) {
+    const AsyncOutcome o = k_async_finish(c, nep, cfg.monitor_loss ? loss_out : nullptr);
+    const uint32_t done = (o.failed || o.stalled) ? o.slot : nep;
+    attr += c.nnz * done;  // one-hop: every arc once per epoch (trainer.cpp:154-160)
+    rep += uint64_t(n) * s * done;
+    if (counters) {
+      counters->attractive_evals += attr;
+      counters->repulsive_evals += rep;
+    }
+    if (o.stalled)
+      fail(F2V_ECUDA, "a Znew row never arrived within the 60 s poll deadline; the epoch was "
+                      "abandoned");
+    if (o.failed) {  // Z = the failed epoch's buffer, restored on the device
+      c.cur = znew_of_epoch[o.slot];
+      const uint32_t e = cfg.first_epoch + o.slot;
+      if (failure) {
+        failure->epoch = e;
+        failure->batch = o.step;
+        failure->vertex = o.vertex;
+      }
+      fail(F2V_ENUMERICAL, "non-finite gradient for vertex " + std::to_string(o.vertex) +
+                               " (epoch " + std::to_string(e) + ", batch " +
+                               std::to_string(o.step) + ")");
+    }
+    return;
   }
   if (counters) {
     counters->attractive_evals += attr;
@@ -386,6 +426,8 @@ void f2v_destroy(f2v_ctx* h) {
   } catch (...) {
   }
   for (cudaEvent_t e : c.ev_kernel) cudaEventDestroy(e);
+  for (cudaEvent_t e : c.ev_async) cudaEventDestroy(e);
+  c.runst.release();
   if (c.ev_begin) cudaEventDestroy(c.ev_begin);
   if (c.ev_end) cudaEventDestroy(c.ev_end);
   if (c.stream) cudaStreamDestroy(c.stream);

@@ -30,6 +30,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -227,14 +228,19 @@ __global__ void negs_kernel(uint32_t* __restrict__ out, uint32_t* __restrict__ n
 }
 
 // Znew := the sentinel NaN everywhere (rows become readable once stored).
-__global__ void sentinel_kernel(uint4* __restrict__ z, uint64_t n16) {
+// After a failed epoch of a back-to-back call, later fills must not touch
+// the restored embedding (stop).
+__global__ void sentinel_kernel(uint4* __restrict__ z, uint64_t n16, const uint32_t* stop) {
+  if (stop && *stop) return;
   const uint4 s = make_uint4(kSentinel, kSentinel, kSentinel, kSentinel);
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
        i += uint64_t(gridDim.x) * blockDim.x)
     __stcg(z + i, s);
 }
 
-__global__ void sentinel_tail_kernel(float* __restrict__ z, uint64_t from, uint64_t to) {
+__global__ void sentinel_tail_kernel(float* __restrict__ z, uint64_t from, uint64_t to,
+                                     const uint32_t* stop) {
+  if (stop && *stop) return;
   const uint64_t i = from + uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < to) z[i] = __uint_as_float(kSentinel);
 }
@@ -257,6 +263,54 @@ __global__ void replica_diff_kernel(const uint32_t* __restrict__ a, const uint32
        i += uint64_t(gridDim.x) * blockDim.x)
     c += a[i] != b[i];
   if (c) atomicAdd(diff, c);
+}
+
+// Back-to-back epochs: the run record (k_async_begin).
+struct RunRecord {
+  uint32_t stop, slot, vertex, stalled;
+  unsigned long long pos, step;
+  double loss[1];  // one per epoch slot
+};
+
+// After an epoch of a back-to-back call: its loss into its slot; a failure
+// (first non-finite position) -> its step (binary search of the combined
+// layout), vertex, stop every later kernel.  One thread.
+__global__ void epoch_done_kernel(const uint32_t* __restrict__ ctr, RunRecord* rec, uint32_t slot,
+                                  const uint32_t* __restrict__ poff, uint32_t T, uint32_t G,
+                                  const uint32_t* __restrict__ perm, int monitor) {
+  if (rec->stop) return;
+  const unsigned long long bad = *reinterpret_cast<const unsigned long long*>(ctr + 2);
+  if (monitor) rec->loss[slot] = *reinterpret_cast<const double*>(ctr + 4);
+  if (ctr[6]) {  // a row poll hit its deadline
+    rec->stalled = 1;
+    rec->slot = slot;
+    rec->stop = 1;
+    return;
+  }
+  if (bad == ~0ull) return;
+  uint32_t lo = 0, hi = T;  // last step t with poff[t G] <= bad
+  while (hi - lo > 1) {
+    const uint32_t m = (lo + hi) / 2;
+    if (poff[size_t(m) * G] <= bad) lo = m;
+    else hi = m;
+  }
+  rec->slot = slot;
+  rec->pos = bad;
+  rec->step = lo;
+  rec->vertex = perm[bad];
+  rec->stop = 1;
+}
+
+// the failed epoch's rows of steps >= the failing one back to Zold (the
+// restore of trainer.cpp:149-152 semantics, on the device)
+__global__ void restore_async_kernel(const uint32_t* __restrict__ state,
+                                     const float* __restrict__ zold, float* __restrict__ znew,
+                                     uint32_t n, uint32_t d, const RunRecord* rec, uint32_t slot) {
+  if (!rec->stop || rec->stalled || rec->slot != slot) return;
+  const uint64_t jb = rec->step;
+  for (uint64_t t = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < uint64_t(n) * d;
+       t += uint64_t(gridDim.x) * blockDim.x)
+    if ((state[t / d] >> 1) >= jb) znew[t] = zold[t];
 }
 
 __global__ void zero_kernel(double* __restrict__ v, uint64_t m) {
@@ -556,8 +610,49 @@ void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sample
   c.launches += 7;
 }
 
-EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bool monitor) {
+void k_async_begin(Ctx& c, uint32_t nslots) {
+  c.runst.ensure(sizeof(RunRecord) + sizeof(double) * nslots);
+  F2V_CUDA(cudaMemsetAsync(c.runst.p, 0, sizeof(RunRecord) + sizeof(double) * nslots, c.stream));
+  while (c.ev_async.size() < 2 * size_t(nslots)) {
+    cudaEvent_t e;
+    F2V_CUDA(cudaEventCreate(&e));
+    c.ev_async.push_back(e);
+  }
+}
+
+AsyncOutcome k_async_finish(Ctx& c, uint32_t nslots, double* loss_out) {
+  std::vector<uint8_t> host(sizeof(RunRecord) + sizeof(double) * nslots);
+  F2V_CUDA(cudaMemcpyAsync(host.data(), c.runst.p, host.size(), cudaMemcpyDeviceToHost,
+                           c.stream));
+  F2V_CUDA(cudaStreamSynchronize(c.stream));
+  RunRecord rec;
+  std::memcpy(&rec, host.data(), sizeof(RunRecord));
+  AsyncOutcome o;
+  o.failed = rec.stop != 0 && !rec.stalled;
+  o.stalled = rec.stalled != 0;
+  o.slot = rec.slot;
+  o.vertex = rec.vertex;
+  o.step = rec.step;
+  o.pos = rec.pos;
+  const uint32_t done = rec.stop ? rec.slot : nslots;  // epochs that completed
+  if (loss_out)
+    std::memcpy(loss_out, host.data() + offsetof(RunRecord, loss), sizeof(double) * done);
+  for (uint32_t e = 0; e < std::min(done + 1, nslots); ++e) {  // epoch kernel times
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c.ev_async[2 * e], c.ev_async[2 * e + 1]) == cudaSuccess) {
+      c.timing[1] += ms;
+      c.timing[2] += 1;
+    }
+  }
+  cudaGetLastError();  // an unrecorded pair (epochs after a failure) is not an error
+  return o;
+}
+
+EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bool monitor,
+                        int async_slot) {
   const int nxt = 1 - c.cur;
+  const bool async = async_slot >= 0;
+  const uint32_t* stop = async ? c.runst.as<uint32_t>() : nullptr;
   const bool multi = c.shard_ready;  // attached (also world 1: exercises the barrier path)
   c.z[nxt].ensure(sizeof(float) * size_t(c.n) * c.d);
   uint32_t* ctr = c.counters.as<uint32_t>();  // [0..1] claims, [2..3] bad, [4..5] loss, [8] nL, [9] nE
@@ -583,9 +678,9 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   auto fill_one = [&](float* z) {  // := sentinel (cudaMalloc'd buffers are 256-byte aligned)
     const uint64_t total = uint64_t(c.n) * c.d, n16 = total / 4;
     sentinel_kernel<<<uint32_t(std::min<uint64_t>((n16 + 255) / 256, 4u * c.num_sms * 8)), 256, 0,
-                      c.stream>>>(reinterpret_cast<uint4*>(z), n16);
+                      c.stream>>>(reinterpret_cast<uint4*>(z), n16, stop);
     F2V_LAUNCHED(c.stream, "sentinel_kernel");
-    if (total % 4) sentinel_tail_kernel<<<1, 4, 0, c.stream>>>(z, n16 * 4, total);
+    if (total % 4) sentinel_tail_kernel<<<1, 4, 0, c.stream>>>(z, n16 * 4, total, stop);
     c.launches += 1;
   };
   auto fill_sentinel = [&] {
@@ -657,6 +752,7 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   a.lslots = c.lslots;
   a.trace = nullptr;
   a.ltrace = nullptr;
+  a.stop = stop;
   if (debug_env("F2V_TRACE")) {
     const uint32_t nbt = c.steps;
     c.trace.ensure(sizeof(unsigned long long) * (5ull * std::max<uint32_t>(c.n, 1) + 3ull * nbt + 2));
@@ -694,9 +790,11 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
   }
   if (tunable && !c.tune.lwarps_env) a.lwarps = c.occ_lwarps;
   auto launch_timed = [&]() {
-    F2V_CUDA(cudaEventRecord(c.ev_kernel[0], c.stream));
+    cudaEvent_t e0 = async ? c.ev_async[2 * async_slot] : c.ev_kernel[0];
+    cudaEvent_t e1 = async ? c.ev_async[2 * async_slot + 1] : c.ev_kernel[1];
+    F2V_CUDA(cudaEventRecord(e0, c.stream));
     ep::launch_epoch(c, a, monitor, c.tune.fast != 0);
-    F2V_CUDA(cudaEventRecord(c.ev_kernel[1], c.stream));
+    F2V_CUDA(cudaEventRecord(e1, c.stream));
   };
   if (tune_now) {
     struct Variant {
@@ -728,9 +826,11 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
       c.occ_use = vv[v].minb;
       a.lwarps = vv[v].lwarps;
       launch_timed();
-      F2V_CUDA(cudaEventSynchronize(c.ev_kernel[1]));
+      cudaEvent_t e0 = async ? c.ev_async[2 * async_slot] : c.ev_kernel[0];
+      cudaEvent_t e1 = async ? c.ev_async[2 * async_slot + 1] : c.ev_kernel[1];
+      F2V_CUDA(cudaEventSynchronize(e1));
       float ms = 0.f;
-      F2V_CUDA(cudaEventElapsedTime(&ms, c.ev_kernel[0], c.ev_kernel[1]));
+      F2V_CUDA(cudaEventElapsedTime(&ms, e0, e1));
       if (v < 2) c.occ_ms[v] = ms;
       if (std::getenv("F2V_DEBUG_OCC"))
         std::fprintf(stderr, "f2v autotune: %d CTAs/SM, %u L warps: %.3f ms\n", vv[v].minb,
@@ -751,6 +851,21 @@ EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bo
                                          reinterpret_cast<double*>(ctr + 4));
     F2V_LAUNCHED(c.stream, "sum_kernel");
     ++c.launches;
+  }
+  if (async) {
+    // the outcome stays on the device: no host round trip between epochs
+    RunRecord* rec = c.runst.as<RunRecord>();
+    epoch_done_kernel<<<1, 1, 0, c.stream>>>(ctr, rec, uint32_t(async_slot), c.poff.as<uint32_t>(),
+                                             c.steps, c.shards, c.perm.as<uint32_t>(),
+                                             monitor ? 1 : 0);
+    F2V_LAUNCHED(c.stream, "epoch_done_kernel");
+    restore_async_kernel<<<4u * c.num_sms, 256, 0, c.stream>>>(
+        c.state.as<uint32_t>(), c.z[c.cur].as<float>(), c.z[nxt].as<float>(), c.n, c.d, rec,
+        uint32_t(async_slot));
+    F2V_LAUNCHED(c.stream, "restore_async_kernel");
+    c.launches += 2;
+    c.cur = nxt;
+    return EpochResult{~0ull, 0.0};
   }
   uint64_t host[5];
   F2V_CUDA(cudaMemcpyAsync(host, ctr, 40, cudaMemcpyDeviceToHost, c.stream));

@@ -82,6 +82,7 @@ struct EpochArgs {
   float eta;
   ForceParams fp;
   uint64_t nnz, chunks, lslots;  // bounds, used by F2V_DEVICE_CHECKS builds
+  const uint32_t* stop;         // back-to-back epochs: an earlier epoch failed -> no work
   int nodep;                    // DEBUG (F2V_DEBUG_NODEP): every row read from Zold, no waits
   unsigned long long* trace;    // DEBUG (F2V_TRACE): per position finalise time (ns)
   unsigned long long* ltrace;   // DEBUG (F2V_TRACE): per position L-item stage times (4 x ns)
@@ -145,7 +146,11 @@ __device__ __forceinline__ float* znew_of(const EpochArgs& a, uint32_t u) {
 
 // Per-warp FIFO of packed row ids (bit 31 = Znew) in shared memory; rows
 // are accumulated 32 at a time in push order (= the deterministic pair order).
-template <int KIND, int K, bool VEC, bool MON, bool FAST, bool ATT>
+#ifndef F2V_INLINE_E
+#define F2V_INLINE_E 0  // E items: the row function inlined at their queue (1) or called (0)
+#endif
+
+template <int KIND, int K, bool VEC, bool MON, bool FAST, bool ATT, bool INL = false>
 struct RowQueue {
   uint32_t* buf;
   int n;
@@ -163,8 +168,12 @@ struct RowQueue {
       buf[lane] = rest;
       __syncwarp();
       n -= 32;
-      Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, 32, lane, a.d, a.zold, zn, zu,
-                                                       acc, lsum);
+      if constexpr (INL)
+        Rows<KIND, K, VEC, MON, FAST>::template run_inl<ATT>(a.fp, pk, 32, lane, a.d, a.zold, zn,
+                                                             zu, acc, lsum);
+      else
+        Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, 32, lane, a.d, a.zold, zn, zu,
+                                                         acc, lsum);
     }
   }
   __device__ __forceinline__ void flush(const EpochArgs& a, int lane, const float (&zu)[K],
@@ -174,8 +183,12 @@ struct RowQueue {
     __syncwarp();
     const int cnt = n;
     n = 0;
-    Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, cnt, lane, a.d, a.zold, zn, zu,
-                                                     acc, lsum);
+    if constexpr (INL)
+      Rows<KIND, K, VEC, MON, FAST>::template run_inl<ATT>(a.fp, pk, cnt, lane, a.d, a.zold, zn, zu,
+                                                           acc, lsum);
+    else
+      Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, cnt, lane, a.d, a.zold, zn, zu,
+                                                       acc, lsum);
   }
 };
 
@@ -263,7 +276,7 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   double lsum = 0.0;
   uint32_t wc = 0;
   float* zn = znew_of(a, u);
-  RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0, zn};
+  RowQueue<KIND, K, VEC, MON, FAST, true, F2V_INLINE_E != 0> q{qbuf, 0, zn};
   // Software pipeline over the chunk's 32-arc groups: while group i's rows
   // are gathered and reduced, group i+1's states and group i+2's column ids
   // are already in flight (the col -> state -> row chain is three dependent
@@ -526,6 +539,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) epoch_kernel(EpochArgs a) {
   uint32_t* rbuf = rs[w];
   if (uses_ring<K, VEC, FAST>()) ring_init(lane);
   const bool lrole = w >= kWarps - int(a.lwarps);
+  if (a.stop && ld_relaxed(a.stop)) return;  // an earlier epoch of this call failed
   uint32_t* counter = a.next + (lrole ? 1 : 0);
   const uint32_t total = lrole ? *a.n_litems : *a.n_eitems_dev;
   uint32_t it = 0;

@@ -134,6 +134,10 @@ struct Ctx {
   DeviceBuf trace;  // DEBUG: per-position finalise timestamps (F2V_TRACE)
   DeviceBuf shufR, shufL;  // device Fisher-Yates (f2v_perm.cu)
 
+  // back-to-back epochs (k_async_begin): the device run record and one
+  // event pair per epoch kernel
+  DeviceBuf runst;
+  std::vector<cudaEvent_t> ev_async;
   // timing of the last train_epochs call (f2v_last_timing)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   std::vector<cudaEvent_t> ev_kernel;  // pairs around each epoch kernel
@@ -153,13 +157,25 @@ struct EpochResult {
   uint64_t bad_pos;
   double loss;
 };
+// Epochs of one f2v_train_epochs call run back to back with no host sync
+// (k_epoch_run with slot >= 0): each epoch's outcome lands in a device run
+// record; the first failure stops every later kernel and restores Z on the
+// device; the host reads the record once at the end (k_async_finish).
+struct AsyncOutcome {
+  bool failed = false, stalled = false;
+  uint32_t slot = 0, vertex = 0;
+  uint64_t step = 0, pos = 0;
+};
+void k_async_begin(Ctx& c, uint32_t nslots);
+AsyncOutcome k_async_finish(Ctx& c, uint32_t nslots, double* loss_out);
 void k_prepare_graph(Ctx& c);
 void k_shard_layout(Ctx& c, uint32_t batch, uint32_t G, uint32_t s);
 void k_epoch_perm(Ctx& c, uint32_t epoch, uint64_t seed);
 void k_epoch_begin(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sampler);
 void k_set_context(Ctx& c, uint32_t walk_k);   // f2v_walk.cu
 void k_epoch_walks(Ctx& c, uint32_t epoch, uint64_t seed);
-EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bool monitor);
+EpochResult k_epoch_run(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bool monitor,
+                        int async_slot = -1);
 void k_epoch_restore(Ctx& c, uint64_t bad_step);
 void k_device_partition(Ctx& c, uint32_t n, uint64_t seed, uint32_t epoch, uint32_t* perm_out);
 void k_device_partition_keyed(Ctx& c, uint32_t n, uint64_t s0, uint32_t* perm_out);

@@ -63,11 +63,13 @@ __device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// force_kernels.hpp:25-29
+// force_kernels.hpp:25-29: x >= 0 -> 1 / (1 + e^-x), else e^x / (1 + e^x).
+// Both branches are n / (1 + e) with e = exp(-|x|) (the same exp argument and
+// the same two roundings), so one exp and one division serve both: the hot
+// EXACT row function is instruction-fetch sensitive.
 __device__ __forceinline__ double stable_sigmoid(double x) {
-  if (x >= 0) return __ddiv_rn(1.0, __dadd_rn(1.0, exp(-x)));
-  const double e = exp(x);
-  return __ddiv_rn(e, __dadd_rn(1.0, e));
+  const double e = exp(-fabs(x));
+  return __ddiv_rn(x >= 0 ? 1.0 : e, __dadd_rn(1.0, e));
 }
 
 __device__ __forceinline__ double dmax(double a, double b) { return (a < b) ? b : a; }
@@ -591,6 +593,10 @@ __device__ __forceinline__ void fast_block(const ForceParams& fp, int k0, int cn
   for (int k = 0; k < K; ++k) acc[k] = __dadd_rn(acc[k], double(a32[k]));
 }
 
+#ifndef F2V_EXACT_REUSE
+#define F2V_EXACT_REUSE 0  // EXACT: keep the block's rows converted to fp64 for the accumulate
+#endif
+
 #ifndef F2V_EXACT_PIPE
 #define F2V_EXACT_PIPE 0  // EXACT: gather the next 8-row block during this one's math
 #endif
@@ -773,12 +779,18 @@ __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t pack
     // products of two floats are exact in fp64, so fma(u, o, s) rounds exactly
     // like the reference's separate multiply and add (force_kernels.cpp:30-34).
     double part[8], nrm[8];
+#if F2V_EXACT_REUSE
+    double ov[8][K];  // the converted rows, reused by the accumulate (one F2F per element)
+#endif
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       double s = 0.0, q = 0.0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const double o = double(v[i][k]);
+#if F2V_EXACT_REUSE
+        ov[i][k] = o;
+#endif
         if (SIG) {
           s = __fma_rn(uu[k], o, s);
           if (!ATT) q = __fma_rn(o, o, q);
@@ -808,7 +820,11 @@ __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t pack
       if (SIG) {  // out_j = c z_j (x scale): scale_into + clamp_magnitude
 #pragma unroll
         for (int k = 0; k < K; ++k) {
+#if F2V_EXACT_REUSE
+          double o = __dmul_rn(c, ov[i][k]);
+#else
           double o = __dmul_rn(c, double(v[i][k]));
+#endif
           if (SCALED && (f & 2)) o = __dmul_rn(o, si);
           acc[k] = __dadd_rn(acc[k], o);
         }
@@ -969,14 +985,16 @@ __device__ __forceinline__ void rows_lowd(const ForceParams& fp, uint32_t packed
   if (lane < int(d)) acc1[0] = __dadd_rn(acc1[0], double(mycol));
 }
 
-// The row-accumulation policy the epoch kernel is instantiated with.
+// The row-accumulation policy the epoch kernel is instantiated with.  run is
+// out of line (one copy per (kind, attractive): the kernel is instruction-
+// fetch sensitive); run_inl is the same body inlined at a hot call site.
 template <int KIND, int K, bool VEC, bool MON, bool FAST>
 struct Rows {
   template <bool ATT>
-  __device__ static __noinline__ void run(const ForceParams& fp, uint32_t packed, int cnt,
-                                             int lane, uint32_t d, const float* zold,
-                                             const float* znew, const float (&zu)[K],
-                                             double (&acc)[K], double& lsum) {
+  __device__ static __forceinline__ void run_inl(const ForceParams& fp, uint32_t packed, int cnt,
+                                                 int lane, uint32_t d, const float* zold,
+                                                 const float* znew, const float (&zu)[K],
+                                                 double (&acc)[K], double& lsum) {
     if constexpr (FAST && K == 1 && !VEC)
       rows_lowd<KIND, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else if constexpr (FAST)
@@ -986,6 +1004,13 @@ struct Rows {
     else
       rows_exact<KIND, K, VEC, 4, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc,
                                             lsum);
+  }
+  template <bool ATT>
+  __device__ static __noinline__ void run(const ForceParams& fp, uint32_t packed, int cnt,
+                                          int lane, uint32_t d, const float* zold,
+                                          const float* znew, const float (&zu)[K],
+                                          double (&acc)[K], double& lsum) {
+    run_inl<ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
   }
 };
 
