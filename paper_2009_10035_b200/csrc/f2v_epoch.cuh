@@ -129,8 +129,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 __device__ __forceinline__ uint32_t lanemask_lt(int lane) { return (1u << lane) - 1u; }
 
 // shard g owns rows [lo[g], lo[g+1]) (orc_shard_layout; G <= kMaxShards)
+// (not unrolled: an unrolled scan over the kernel-parameter array cost ~700
+// instructions and ~90 local loads in the epoch kernel, which is instruction-
+// fetch sensitive; it runs only for G > 1)
 __device__ __forceinline__ uint32_t shard_of(uint32_t u, const uint32_t* lo, uint32_t G) {
   uint32_t g = 0;
+#pragma unroll 1
   for (uint32_t i = 1; i < G; ++i) g += u >= lo[i] ? 1u : 0u;
   return g;
 }
@@ -140,21 +144,33 @@ __device__ __forceinline__ uint32_t neg_set(const EpochArgs& a, uint32_t u, uint
 }
 
 // the Znew replica the items of vertex u read and publish into
+// (EMUL: the replica-emulation instantiation, f2v_epoch_i_emul.cu; the
+// production kernels carry none of it -- it cost C2 ~7% as a run-time branch)
+template <bool EMUL>
 __device__ __forceinline__ float* znew_of(const EpochArgs& a, uint32_t u) {
-  return a.emul ? a.rep_znew[shard_of(u, a.shard_lo, a.shards)] : a.znew;
+  if constexpr (EMUL) return a.rep_znew[shard_of(u, a.shard_lo, a.shards)];
+  (void)u;
+  return a.znew;
 }
 
 // Per-warp FIFO of packed row ids (bit 31 = Znew) in shared memory; rows
 // are accumulated 32 at a time in push order (= the deterministic pair order).
+#ifndef F2V_E_PREFETCH
+// E items: the next groups' column ids / states in flight while this group's
+// rows are reduced.  Measured slower (same box: C3 FAST 28.9 -> 29.5 ms, C3
+// EXACT 50.2 -> 52.1 ms: the extra registers live across the row calls), off.
+#define F2V_E_PREFETCH 0
+#endif
+
 #ifndef F2V_INLINE_E
 #define F2V_INLINE_E 0  // E items: the row function inlined at their queue (1) or called (0)
 #endif
 
-template <int KIND, int K, bool VEC, bool MON, bool FAST, bool ATT, bool INL = false>
+template <int KIND, int K, bool VEC, bool MON, bool FAST, bool ATT, bool EMUL, bool INL = false>
 struct RowQueue {
   uint32_t* buf;
   int n;
-  const float* zn;  // the Znew replica of the item
+  const float* zn;  // the Znew replica of the item (EMUL; else a.znew, reloaded per call)
   __device__ __forceinline__ void push(const EpochArgs& a, int lane, bool keep, uint32_t val,
                                        const float (&zu)[K], double (&acc)[K], double& lsum) {
     const uint32_t m = __ballot_sync(kFull, keep);
@@ -169,11 +185,11 @@ struct RowQueue {
       __syncwarp();
       n -= 32;
       if constexpr (INL)
-        Rows<KIND, K, VEC, MON, FAST>::template run_inl<ATT>(a.fp, pk, 32, lane, a.d, a.zold, zn,
-                                                             zu, acc, lsum);
+        Rows<KIND, K, VEC, MON, FAST>::template run_inl<ATT>(a.fp, pk, 32, lane, a.d, a.zold,
+                                                             EMUL ? zn : a.znew, zu, acc, lsum);
       else
-        Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, 32, lane, a.d, a.zold, zn, zu,
-                                                         acc, lsum);
+        Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, 32, lane, a.d, a.zold,
+                                                         EMUL ? zn : a.znew, zu, acc, lsum);
     }
   }
   __device__ __forceinline__ void flush(const EpochArgs& a, int lane, const float (&zu)[K],
@@ -184,16 +200,16 @@ struct RowQueue {
     const int cnt = n;
     n = 0;
     if constexpr (INL)
-      Rows<KIND, K, VEC, MON, FAST>::template run_inl<ATT>(a.fp, pk, cnt, lane, a.d, a.zold, zn, zu,
-                                                           acc, lsum);
+      Rows<KIND, K, VEC, MON, FAST>::template run_inl<ATT>(a.fp, pk, cnt, lane, a.d, a.zold,
+                                                           EMUL ? zn : a.znew, zu, acc, lsum);
     else
-      Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, cnt, lane, a.d, a.zold, zn, zu,
-                                                       acc, lsum);
+      Rows<KIND, K, VEC, MON, FAST>::template run<ATT>(a.fp, pk, cnt, lane, a.d, a.zold,
+                                                       EMUL ? zn : a.znew, zu, acc, lsum);
   }
 };
 
 // The shared negatives of batch j, in sample order (sampling.cpp:59).
-template <int KIND, int K, bool VEC, bool MON, bool FAST>
+template <int KIND, int K, bool VEC, bool MON, bool FAST, bool EMUL>
 __device__ __forceinline__ void do_negatives(const EpochArgs& a, const float* zn, uint32_t j,
                                              uint32_t q, int lane, const float (&zu)[K],
                                              double (&acc)[K], double& lsum) {
@@ -209,8 +225,8 @@ __device__ __forceinline__ void do_negatives(const EpochArgs& a, const float* zn
         pk = w;
       }
     }
-    Rows<KIND, K, VEC, MON, FAST>::template run<false>(a.fp, pk, cnt, lane, a.d, a.zold, zn, zu,
-                                                       acc, lsum);
+    Rows<KIND, K, VEC, MON, FAST>::template run<false>(a.fp, pk, cnt, lane, a.d, a.zold,
+                                                       EMUL ? zn : a.znew, zu, acc, lsum);
   }
 }
 
@@ -229,7 +245,7 @@ __device__ __noinline__ void store_peers(const EpochArgs& a, const float* zn, ui
 
 // g = float(acc) (trainer.cpp:140-145); z_u -= eta*g in fp32 (trainer.cpp:173);
 // publish row u of Znew.
-template <int K, bool VEC, bool MON>
+template <int K, bool VEC, bool MON, bool EMUL>
 __device__ __forceinline__ void finalize(const EpochArgs& a, float* zn, uint32_t p, uint32_t u,
                                          int lane, const float (&zu)[K], const double (&acc)[K],
                                          double lsum) {
@@ -243,8 +259,8 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, float* zn, uint32_t
     nz[k] = __fsub_rn(zu[k], __fmul_rn(a.eta, g));
     if (nz[k] != nz[k]) nz[k] = __int_as_float(0x7fffffff);  // never the sentinel NaN
   }
-  L::store(zn + size_t(u) * a.d, lane, a.d, nz);  // publishes the row (sentinel-free)
-  if (a.npeers | a.emul) store_peers<K, VEC>(a, zn, u, lane, nz);  // peers' replicas (NVLink)
+  L::store((EMUL ? zn : a.znew) + size_t(u) * a.d, lane, a.d, nz);  // publishes the row
+  if (EMUL || a.npeers) store_peers<K, VEC>(a, zn, u, lane, nz);  // peers' replicas (NVLink)
   const bool any_bad = __any_sync(kFull, bad);
   if (MON) {
     const double tot = warp_sum_d(lsum);
@@ -256,7 +272,7 @@ __device__ __forceinline__ void finalize(const EpochArgs& a, float* zn, uint32_t
   }
 }
 
-template <int KIND, int K, bool VEC, bool MON, bool FAST>
+template <int KIND, int K, bool VEC, bool MON, bool FAST, bool EMUL>
 __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* qbuf) {
   using L = Lay<K, VEC>;
   const uint32_t p = item.p, u = item.u, cb = item.cb, c = item.c, nch = item.nch;
@@ -275,23 +291,30 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   for (int k = 0; k < K; ++k) acc[k] = 0.0;
   double lsum = 0.0;
   uint32_t wc = 0;
-  float* zn = znew_of(a, u);
-  RowQueue<KIND, K, VEC, MON, FAST, true, F2V_INLINE_E != 0> q{qbuf, 0, zn};
+  float* zn = znew_of<EMUL>(a, u);
+  RowQueue<KIND, K, VEC, MON, FAST, true, EMUL, F2V_INLINE_E != 0> q{qbuf, 0, zn};
   // Software pipeline over the chunk's 32-arc groups: while group i's rows
   // are gathered and reduced, group i+1's states and group i+2's column ids
   // are already in flight (the col -> state -> row chain is three dependent
   // loads per arc).
+#if F2V_E_PREFETCH
   uint32_t v_cur = e0 + lane < e1 ? __ldg(a.col + e0 + lane) : 0u;  // this group's ids
   uint32_t v_nx = e0 + 32 + lane < e1 ? __ldg(a.col + e0 + 32 + lane) : 0u;  // the next's
   uint32_t st_cur = e0 + lane < e1 ? ld_relaxed(a.state + v_cur) : 0u;  // this group's states
+#endif
   for (uint64_t e = e0; e < e1; e += 32) {
     const int cnt = int(umin64(32, e1 - e));
+#if F2V_E_PREFETCH
     const uint32_t v = v_cur, st = st_cur;
-    uint32_t pk = 0;
     // issue the next group's states and the group after's column ids
     st_cur = e + 32 + lane < e1 ? ld_relaxed(a.state + v_nx) : 0u;
     v_cur = v_nx;
     v_nx = e + 64 + lane < e1 ? __ldg(a.col + e + 64 + lane) : 0u;
+#else
+    const uint32_t v = lane < cnt ? a.col[e + lane] : 0u;
+    const uint32_t st = lane < cnt ? ld_relaxed(a.state + v) : 0u;
+#endif
+    uint32_t pk = 0;
     bool use = false, win = false;
     if (lane < cnt) {
       DCHECK(e + lane < a.nnz, "E arc %llu nnz %llu", (unsigned long long)(e + lane),
@@ -318,8 +341,8 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   const bool needs = a.needs[u] != 0;
   if (nch == 1) {
     if (!needs) {
-      do_negatives<KIND, K, VEC, MON, FAST>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
-      finalize<K, VEC, MON>(a, zn, p, u, lane, zu, acc, lsum);
+      do_negatives<KIND, K, VEC, MON, FAST, EMUL>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
+      finalize<K, VEC, MON, EMUL>(a, zn, p, u, lane, zu, acc, lsum);
     } else {
       L::store_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);
       const double ls = MON ? warp_sum_d(lsum) : 0.0;
@@ -357,8 +380,8 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   }
   if (lane == 0) a.ecnt[u] = 0;
   if (!needs) {
-    do_negatives<KIND, K, VEC, MON, FAST>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
-    finalize<K, VEC, MON>(a, zn, p, u, lane, zu, acc, lsum);
+    do_negatives<KIND, K, VEC, MON, FAST, EMUL>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
+    finalize<K, VEC, MON, EMUL>(a, zn, p, u, lane, zu, acc, lsum);
   } else {
     L::store_acc(a.epart + size_t(ps) * a.d, lane, a.d, acc);  // the E total
     if (MON && lane == 0) __stcg(a.eloss + cb, lsum);  // lane 0 holds the whole sum here
@@ -369,7 +392,7 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
 }
 
 // Take the parked recent window arcs in order, waiting on each row.
-template <int KIND, int K, bool VEC, bool MON, bool FAST>
+template <int KIND, int K, bool VEC, bool MON, bool FAST, bool EMUL>
 __device__ __forceinline__ void recent_pass(const EpochArgs& a, const float* zn, int lane,
                                             uint32_t* rbuf, int& nr, const float (&zu)[K],
                                             double (&acc)[K], double& lsum) {
@@ -380,8 +403,8 @@ __device__ __forceinline__ void recent_pass(const EpochArgs& a, const float* zn,
       const uint32_t v = rbuf[t0 + lane];
       pk = v | kNewBit;
     }
-    Rows<KIND, K, VEC, MON, FAST>::template run<true>(a.fp, pk, cnt, lane, a.d, a.zold, zn, zu,
-                                                      acc, lsum);
+    Rows<KIND, K, VEC, MON, FAST>::template run<true>(a.fp, pk, cnt, lane, a.d, a.zold,
+                                                      EMUL ? zn : a.znew, zu, acc, lsum);
   }
   __syncwarp();
   nr = 0;
@@ -392,7 +415,7 @@ __device__ __forceinline__ void recent_pass(const EpochArgs& a, const float* zn,
 // straight into the row queue; the most recent ones are parked in rbuf and
 // taken last (recent_pass) so the dependency tail of the item is short.  The
 // order is a function of the data only (deterministic).
-template <int KIND, int K, bool VEC, bool MON, bool FAST>
+template <int KIND, int K, bool VEC, bool MON, bool FAST, bool EMUL>
 __device__ __forceinline__ void window_collect(const EpochArgs& a, const float* zn, uint32_t u,
                                                uint32_t j, uint32_t c0, uint32_t c1, int lane,
                                                uint32_t* qbuf, uint32_t* rbuf, int& nr,
@@ -400,7 +423,7 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, const float* 
                                                double& lsum) {
   const uint64_t r0 = a.rowptr[u];
   const uint32_t cb = a.cbase[u];
-  RowQueue<KIND, K, VEC, MON, FAST, true> q{qbuf, 0, zn};
+  RowQueue<KIND, K, VEC, MON, FAST, true, EMUL> q{qbuf, 0, zn};
   for (uint32_t cc = c0; cc < c1; cc += 32) {
     const uint32_t nc = umin32(32, c1 - cc);
     const uint32_t mine = lane < int(nc) ? __ldcg(a.wcnt + cb + cc + lane) : 0u;
@@ -441,7 +464,7 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, const float* 
       // park the recent ones (processed in place if the parking lot is full)
       if (nr + __popc(rm) > kRq) {
         q.flush(a, lane, zu, acc, lsum);
-        recent_pass<KIND, K, VEC, MON, FAST>(a, zn, lane, rbuf, nr, zu, acc, lsum);
+        recent_pass<KIND, K, VEC, MON, FAST, EMUL>(a, zn, lane, rbuf, nr, zu, acc, lsum);
       }
       if (recent) rbuf[nr + __popc(rm & lanemask_lt(lane))] = v;
       __syncwarp();
@@ -451,7 +474,7 @@ __device__ __forceinline__ void window_collect(const EpochArgs& a, const float* 
   q.flush(a, lane, zu, acc, lsum);
 }
 
-template <int KIND, int K, bool VEC, bool MON, bool FAST>
+template <int KIND, int K, bool VEC, bool MON, bool FAST, bool EMUL>
 __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint32_t* qbuf,
                      uint32_t* rbuf) {
   using L = Lay<K, VEC>;
@@ -466,7 +489,7 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
   unsigned long long* lt = (a.ltrace && cl == 0) ? a.ltrace + 4ull * p : nullptr;
 #endif
   if (lane == 0) F2V_STAMP(lt, 0);
-  float* zn = znew_of(a, u);
+  float* zn = znew_of<EMUL>(a, u);
   float zu[K];
   L::load(a.zold + size_t(u) * a.d, lane, a.d, zu, false);
   double acc[K];
@@ -487,20 +510,20 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     if (MON && lane == 0) lsum = __ldcg(a.eloss + cb);
     int nr = 0;
     // E total + old window arcs + negatives + recent arcs
-    window_collect<KIND, K, VEC, MON, FAST>(a, zn, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
+    window_collect<KIND, K, VEC, MON, FAST, EMUL>(a, zn, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
                                             lsum);
-    do_negatives<KIND, K, VEC, MON, FAST>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
+    do_negatives<KIND, K, VEC, MON, FAST, EMUL>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
     if (lane == 0) F2V_STAMP(lt, 2);
-    recent_pass<KIND, K, VEC, MON, FAST>(a, zn, lane, rbuf, nr, zu, acc, lsum);
+    recent_pass<KIND, K, VEC, MON, FAST, EMUL>(a, zn, lane, rbuf, nr, zu, acc, lsum);
     if (lane == 0) F2V_STAMP(lt, 3);
-    finalize<K, VEC, MON>(a, zn, p, u, lane, zu, acc, lsum);
+    finalize<K, VEC, MON, EMUL>(a, zn, p, u, lane, zu, acc, lsum);
     if (lane == 0) a.vflag[u] = 0;
     return;
   }
   int nr = 0;
-  window_collect<KIND, K, VEC, MON, FAST>(a, zn, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
+  window_collect<KIND, K, VEC, MON, FAST, EMUL>(a, zn, u, j, c0, c1, lane, qbuf, rbuf, nr, zu, acc,
                                           lsum);
-  recent_pass<KIND, K, VEC, MON, FAST>(a, zn, lane, rbuf, nr, zu, acc, lsum);
+  recent_pass<KIND, K, VEC, MON, FAST, EMUL>(a, zn, lane, rbuf, nr, zu, acc, lsum);
   const uint32_t slot = a.lpo[u] + cl;
   DCHECK(slot < a.lslots, "L slot=%u lslots=%llu cl=%u nchL=%u", slot,
          (unsigned long long)a.lslots, cl, nchL);
@@ -523,13 +546,13 @@ __device__ void do_L(const EpochArgs& a, uint32_t p, uint32_t cl, int lane, uint
     L::add_acc(a.lpart + size_t(lp + qq) * a.d, lane, a.d, acc);
     if (MON && lane == 0) lsum = __dadd_rn(lsum, __ldcg(a.lloss + lp + qq));
   }
-  do_negatives<KIND, K, VEC, MON, FAST>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
+  do_negatives<KIND, K, VEC, MON, FAST, EMUL>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);
   if (lane == 0) a.lcnt[u] = 0;
-  finalize<K, VEC, MON>(a, zn, p, u, lane, zu, acc, lsum);
+  finalize<K, VEC, MON, EMUL>(a, zn, p, u, lane, zu, acc, lsum);
   if (lane == 0) a.vflag[u] = 0;
 }
 
-template <int KIND, int K, bool VEC, bool MON, bool FAST, int MINB>
+template <int KIND, int K, bool VEC, bool MON, bool FAST, int MINB, bool EMUL = false>
 __global__ void __launch_bounds__(kWarps * 32, MINB) epoch_kernel(EpochArgs a) {
   __shared__ uint32_t qs[kWarps][kQ];
   __shared__ uint32_t rs[kWarps][kRq];
@@ -551,18 +574,18 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) epoch_kernel(EpochArgs a) {
     if (lane == 0) nxt = atomicAdd(counter, 1u);  // claim ahead: hides the atomic's latency
     if (lrole) {
       const uint2 item = a.litems[it];
-      do_L<KIND, K, VEC, MON, FAST>(a, item.x, item.y, lane, qbuf, rbuf);
+      do_L<KIND, K, VEC, MON, FAST, EMUL>(a, item.x, item.y, lane, qbuf, rbuf);
     } else {
-      do_E<KIND, K, VEC, MON, FAST>(a, a.eitems[it], lane, qbuf);
+      do_E<KIND, K, VEC, MON, FAST, EMUL>(a, a.eitems[it], lane, qbuf);
     }
     it = __shfl_sync(kFull, nxt, 0);
   }
 }
 
 // Launch one epoch kernel instantiation as a persistent grid.
-template <int KIND, int K, bool VEC, bool MON, bool FAST, int MINB>
+template <int KIND, int K, bool VEC, bool MON, bool FAST, int MINB, bool EMUL = false>
 void launch_one(Ctx& c, const EpochArgs& a) {
-  auto kern = epoch_kernel<KIND, K, VEC, MON, FAST, MINB>;
+  auto kern = epoch_kernel<KIND, K, VEC, MON, FAST, MINB, EMUL>;
   const size_t dsmem = uses_ring<K, VEC, FAST>() ? size_t(kWarps) * kRingWarpBytes : 0;
   if (dsmem) F2V_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(dsmem)));
@@ -587,9 +610,14 @@ void launch_one(Ctx& c, const EpochArgs& a) {
 #ifndef F2V_EXACT_MINB
 // EXACT d = 128 register budget (resident 8-warp CTAs per SM).  Register
 // gathers: 3 (80 registers, 24 warps/SM) measured 57.7 ms on C3 against 65.1
-// ms at 2 (128); with the TMA row ring (F2V_ROW_TMA_EXACT) 2 is better: 62.6
-// ms against 75.6 ms at 3 (the ring's shared memory halves the resident L1)
+// ms at 2 (128); with the TMA row ring (F2V_ROW_TMA_EXACT) 2 is better: 56.3
+// ms against 66.5 ms at 3 with one ring stage (the ring's shared memory
+// costs resident L1)
 #define F2V_EXACT_MINB (F2V_ROW_TMA_EXACT ? 2 : 3)
+#endif
+
+#ifndef F2V_FAST_MINB_HI
+#define F2V_FAST_MINB_HI 3  // FAST d = 128: the occupancy autotune's high-occupancy build
 #endif
 
 template <int KIND, int K, bool VEC, bool FAST>
@@ -597,11 +625,16 @@ void launch_mon(Ctx& c, const EpochArgs& a, bool mon) {
   if constexpr (!FAST && K == 4 && VEC) {
     if (mon) launch_one<KIND, K, VEC, true, FAST, F2V_EXACT_MINB>(c, a);
     else launch_one<KIND, K, VEC, false, FAST, F2V_EXACT_MINB>(c, a);
+  } else if constexpr (FAST && K == 1 && !VEC) {
+    // the low-d lane-per-pair path (config 4) is latency-bound: 3 CTAs/SM
+    // (80 registers); at 2 the compiler takes 116 and C4 ran 2.2 -> 3.4 ms
+    if (mon) launch_one<KIND, K, VEC, true, FAST, 3>(c, a);
+    else launch_one<KIND, K, VEC, false, FAST, 3>(c, a);
   } else {
     if constexpr (FAST && K == 4) {
       if (c.occ_use == 3) {
-        if (mon) launch_one<KIND, K, VEC, true, FAST, 3>(c, a);
-        else launch_one<KIND, K, VEC, false, FAST, 3>(c, a);
+        if (mon) launch_one<KIND, K, VEC, true, FAST, F2V_FAST_MINB_HI>(c, a);
+        else launch_one<KIND, K, VEC, false, FAST, F2V_FAST_MINB_HI>(c, a);
         return;
       }
     }
@@ -636,11 +669,16 @@ void launch_exact_any_k4(Ctx& c, const EpochArgs& a, bool mon);
 void launch_exact_any_k8(Ctx& c, const EpochArgs& a, bool mon);
 void launch_exact_any_k16(Ctx& c, const EpochArgs& a, bool mon);
 void launch_exact_any_k32(Ctx& c, const EpochArgs& a, bool mon);
+void launch_emul(Ctx& c, const EpochArgs& a, bool mon, bool fast);  // f2v_epoch_i_emul.cu
 
 // d = 64/128/256 and d <= 4 (lane-per-pair, rows_lowd) run FAST when asked;
 // everything else runs EXACT.
 inline void launch_epoch(Ctx& c, const EpochArgs& a, bool mon, bool fast) {
   const uint32_t d = a.d;
+  if (a.emul) {
+    launch_emul(c, a, mon, fast);
+    return;
+  }
   if (fast && d == 128) launch_fast_k4(c, a, mon);
   else if (fast && d == 64) launch_fast_k2(c, a, mon);
   else if (fast && d == 256) launch_fast_k8(c, a, mon);

@@ -43,13 +43,15 @@ __device__ __forceinline__ bool has_sentinel(const float (&v)[K]) {
   return b;
 }
 
-// Row polls give up after this much wall time (%globaltimer, ns).
-constexpr unsigned long long kPollDeadlineNs = 60ull * 1000 * 1000 * 1000;
-__device__ __forceinline__ bool poll_expired(unsigned long long& t0) {
-  unsigned long long now;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(now));
-  if (!t0) t0 = now;
-  return now - t0 > kPollDeadlineNs;
+// A row poll gives up after kPollLimit iterations (>= 2^28 x 32..256 ns of
+// back-off: about a minute) and raises *stall (the row keeps its sentinel NaN);
+// the host then reports F2V_ECUDA (a stalled or dead peer GPU) instead of the
+// device trapping or hanging.  An iteration count, not %globaltimer: the poll
+// loop is on the batch chain and inlined at every row-block site, and a clock
+// read per iteration (or an out-of-line poll) cost config 2 10-80%.
+constexpr uint32_t kPollLimit = 1u << 28;
+static __device__ __noinline__ void poll_stalled(uint32_t* stall) {
+  if (stall) atomicExch(stall, 1u);
 }
 
 // Relaxed (no L1 invalidation) global loads/stores for cross-warp flags; the
@@ -117,16 +119,12 @@ struct Lay {
                                               float (&v)[K], uint32_t* stall) {
     // exponential back-off (32 ns .. F2V_POLL_MAX_NS): spinning warps would
     // otherwise take issue slots from the warps streaming rows on the same SM
-    uint32_t ns = 32;
-    unsigned long long t0 = 0;
-    while (__any_sync(kFull, has_sentinel<K, (VEC && K % 4 == 0) ? 2 : 1>(v))) {
+    uint32_t ns = 32, it = 0;
+    while (__any_sync(kFull, it < kPollLimit && has_sentinel<K, (VEC && K % 4 == 0) ? 2 : 1>(v))) {
       __nanosleep(ns);
       ns = ns < F2V_POLL_MAX_NS ? 2 * ns : ns;
       load(row, lane, d, v, true);
-      if (poll_expired(t0)) {
-        if (lane == 0 && stall) atomicExch(stall, 1u);
-        break;
-      }
+      if (++it == kPollLimit) poll_stalled(stall);  // give up (the loop ends for every lane)
     }
   }
   __device__ static __forceinline__ void store(float* row, int lane, uint32_t d,
@@ -170,18 +168,22 @@ struct Lay {
 // next block's gathers are in flight -- without registers -- while this
 // block's pair math runs.  The copies read L2 like ld.cg; Znew rows still go
 // through the sentinel check (and the poll on direct loads).
-// Measured and not enabled by default (same box, A/B): FAST C3 30.6 -> 30.4 ms,
-// FAST C2 8.35 -> 9.03 ms (the ring's loads bypass L1, where R-MAT's hub rows
-// hit), EXACT C3 61.4 -> 62.6 ms at 2 CTAs/SM and 75.6 ms at 3 (the fp64 pair
-// math, not the gathers, bounds EXACT; the 128 KB+ carve-out costs L1).
-// Compile with -DF2V_ROW_TMA_EXACT=1 / -DF2V_ROW_TMA_FAST=1 to use it.
+// Same-box A/B measurements (C3 epoch kernel):
+//   EXACT, 1 stage (the next block streams into shared memory while this one
+//   is reduced from registers), 2 CTAs/SM: 58.8 -> 56.3 ms  <- the default
+//   EXACT, 2 stages: 62.6 ms at 2 CTAs/SM, 75.6 ms at 3 (the carve-out halves L1)
+//   FAST, 2 stages: C3 30.6 -> 30.4 ms, C2 8.35 -> 9.03 ms (the bulk copies
+//   bypass L1, where R-MAT's hub rows hit) -- FAST keeps register gathers.
 #ifndef F2V_ROW_TMA_EXACT
-#define F2V_ROW_TMA_EXACT 0
+#define F2V_ROW_TMA_EXACT 1
 #endif
 #ifndef F2V_ROW_TMA_FAST
 #define F2V_ROW_TMA_FAST 0
 #endif
-constexpr int kRingStages = 2;
+#ifndef F2V_RING_STAGES
+#define F2V_RING_STAGES 1  // 1: the next block streams in while this one is reduced from registers
+#endif
+constexpr int kRingStages = F2V_RING_STAGES;
 constexpr uint32_t kRowBytes = 512;  // d = 128 rows (the ring serves the VEC K = 4 layouts)
 constexpr uint32_t kRingWarpBytes = 128 + kRingStages * 8 * kRowBytes;  // barriers + slots
 
@@ -946,16 +948,12 @@ __device__ __forceinline__ void rows_lowd(const ForceParams& fp, uint32_t packed
     for (int c = 0; c < kLowD; ++c) b |= __float_as_uint(w[c]) == kSentinel;
     return b && mine && (pk & kNewBit);
   };
-  uint32_t ns = 32;
-  unsigned long long t0 = 0;
-  while (__any_sync(kFull, pending())) {
+  uint32_t ns = 32, it = 0;
+  while (__any_sync(kFull, it < kPollLimit && pending())) {
     __nanosleep(ns);
     ns = ns < F2V_POLL_MAX_NS ? 2 * ns : ns;
     if (pending()) load();
-    if (poll_expired(t0)) {
-      if (lane == 0 && fp.stall) atomicExch(fp.stall, 1u);
-      break;
-    }
+    if (++it == kPollLimit) poll_stalled(fp.stall);  // give up (the loop ends for every lane)
   }
   float red = 0.f, nrm = 0.f;
 #pragma unroll

@@ -186,8 +186,8 @@ def test_allgather_driver_on_device(f2v, orc, backend):
 
 
 @pytest.mark.parametrize("precision", ["fast", "exact"])
-@pytest.mark.parametrize("G,kind,d", [(2, "sigmoid", 128), (3, "tdist", 128), (8, "tdist", 64),
-                                      (4, "sigmoid", 2)])
+@pytest.mark.parametrize("G,kind,d", [(2, "sigmoid", 128), (3, "tdist", 128), (8, "tdist", 128),
+                                      (4, "sigmoid", 128)])
 def test_emulated_replicas_match_oracle(f2v, orc, dev, precision, G, kind, d):
     """The G-GPU data flow inside ONE launch (the safe stand-in for G GPUs on
     one device): shard g's items read and publish into their own Znew
