@@ -583,12 +583,23 @@ class Device:
 
     # ------------------------------ per-step all-gather baseline (NCCL)
     @staticmethod
+    def _nccl_first():
+        # torch links its own (newer) NCCL under the same soname: it must be the
+        # libnccl.so.2 of this process, so it is loaded before ours resolves one
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
+
+    @staticmethod
     def nccl_unique_id() -> bytes:
+        Device._nccl_first()
         buf = C.create_string_buffer(128)
         _check(_lib.f2v_nccl_unique_id(buf))
         return buf.raw
 
     def nccl_init(self, unique_id: bytes, rank: int, world: int):
+        Device._nccl_first()
         self._ck(_lib.f2v_nccl_init(self._h, unique_id, rank, world))
 
     def train_epochs_allgather(self, cfg: TrainConfig, first_epoch: int = 0,

@@ -10,9 +10,10 @@
 // numbers as the fused NVLink epoch kernel (f2v_epoch.cuh) and orc_train(G);
 // it is the baseline the fused path is measured against.
 //
-// NCCL is loaded at run time (dlopen "libnccl.so.2": torch's bundled NCCL when
-// torch is already in the process, else the system one), so the library has no
-// link-time NCCL dependency; only <nccl.h>'s types are used.
+// NCCL is loaded at run time (dlopen "libnccl.so.2": the one already in the
+// process -- torch's bundled NCCL, which the Python wrapper imports first --
+// else the system one, RTLD_LOCAL), so the library has no link-time NCCL
+// dependency; only <nccl.h>'s types are used.
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -41,9 +42,16 @@ struct NcclApi {
 NcclApi& nccl() {
   static NcclApi api = [] {
     NcclApi a;
+    // an NCCL already in the process first (torch's bundled one, whose newer
+    // symbols torch needs), else the system library -- RTLD_LOCAL either way,
+    // so this library never changes what other code resolves
     for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
-      a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      a.h = dlopen(name, RTLD_NOW | RTLD_LOCAL | RTLD_NOLOAD);
       if (a.h) break;
+    }
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      if (a.h) break;
+      a.h = dlopen(name, RTLD_NOW | RTLD_LOCAL);
     }
     if (!a.h) return a;
     a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(a.h, "ncclGetUniqueId"));

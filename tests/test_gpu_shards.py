@@ -285,3 +285,20 @@ def test_nccl_allgather_library_failure(f2v, orc):
     assert rc == 4
     assert (fail["epoch"], fail["batch"], fail["vertex"]) == tuple(int(x) for x in finfo)
     z_parity(z, zr)
+
+
+def test_nccl_before_torch_import():
+    """The library's NCCL (run-time dlopen) must not shadow torch's bundled
+    NCCL: creating the per-step baseline's communicator before `import torch`
+    left torch unable to resolve its newer NCCL symbols (round-2 bench)."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+    code = ("import sys; sys.path.insert(0, %r); import paper_2009_10035_b200 as f2v; "
+            "uid = f2v.Device.nccl_unique_id(); import torch; "
+            "print('OK', len(uid), torch.cuda.is_available())" % ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().startswith("OK 128"), out.stdout
