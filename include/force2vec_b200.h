@@ -7,7 +7,8 @@
  * exception taxonomy (errors.hpp:8-40, CLI mapping force2vec.cpp:23-26):
  *   F2V_OK 0, F2V_EUSAGE 1 (UsageError), F2V_EIO 2 (IoError),
  *   F2V_ERANGE 3 (FormatError/RangeError), F2V_ENUMERICAL 4 (NumericalError),
- *   F2V_ECUDA 5 (device/driver failure), F2V_EUNSUPPORTED 6 (UnsupportedError).
+ *   F2V_ECUDA 5 (device/driver failure), F2V_EUNSUPPORTED 6 (UnsupportedError),
+ *   F2V_EERROR 7 (the base class Error).
  * f2v_last_error() returns the message the reference would have thrown, e.g.
  * "non-finite gradient for vertex 7 (epoch 0, batch 3)" (trainer.cpp:149-152,
  * 229-233).
@@ -34,6 +35,8 @@ extern "C" {
 #define F2V_ENUMERICAL 4
 #define F2V_ECUDA 5
 #define F2V_EUNSUPPORTED 6
+#define F2V_EERROR 7 /* force2vec::Error itself (errors.hpp:10-12), e.g. fit_logreg's
+                        "degenerate single-class input" */
 
 /* ForceKind, force_kernels.hpp:12 (same order) */
 #define F2V_SIGMOID 0
@@ -264,6 +267,73 @@ int32_t f2v_train_epochs_allgather(f2v_ctx* ctx, const f2v_train_config* cfg, do
  * rows f32[b*d] row-major */
 int32_t f2v_get_rows(f2v_ctx* ctx, const uint32_t* ids, uint32_t b, float* rows_out);
 int32_t f2v_set_rows(f2v_ctx* ctx, const uint32_t* ids, uint32_t b, const float* rows);
+
+/* ------------------------------------------------ after training
+ * Embedding text I/O (embedding_io.cpp:24-100), host side.  The file format is
+ * the reference's: header "n d", then n lines "vertex_id f_1 ... f_d" with the
+ * shortest round-trip decimal of every float, so write + read is bitwise
+ * lossless and files are byte-identical to the reference's.  Errors carry the
+ * reference's messages (f2v_global_error()). */
+int32_t f2v_write_embedding(const char* path, const float* z, uint32_t n, uint32_t d);
+/* *z_out is allocated by the library (f2v_free) */
+int32_t f2v_read_embedding(const char* path, float** z_out, uint32_t* n_out, uint32_t* d_out);
+/* write_layout_tsv (embedding_io.cpp:102-124): "id\tx\ty[\tlabel]", d must be 2;
+ * first_label nullable, -1 = unlabeled */
+int32_t f2v_write_layout_tsv(const char* path, const float* z, uint32_t n, uint32_t d,
+                             const int32_t* first_label);
+
+/* Evaluation (evaluation.cpp) on the device, over the context's graph and its
+ * current embedding.  rng_state is the state word of the reference's Rng
+ * (rng.hpp:12-53: next() adds the Weyl constant and mixes), advanced exactly as
+ * the reference advances it; f2v_rng_state(seed, stream) = Rng(seed, stream). */
+uint64_t f2v_rng_state(uint64_t seed, uint64_t stream);
+/* kmeans (evaluation.cpp:428-438): Lloyd + k-means++ seeding, empty clusters
+ * re-seeded at the farthest point, best of `restarts` by inertia.  The
+ * clustering is bit-identical to the reference's (every fp64 sum in its order). */
+int32_t f2v_kmeans(f2v_ctx* ctx, int32_t k, uint64_t* rng_state, int32_t restarts,
+                   int32_t max_iters, int32_t* assignment_out, double* inertia_out);
+/* kmeans_inertia (evaluation.cpp:440-458) */
+int32_t f2v_kmeans_inertia(f2v_ctx* ctx, int32_t k, const int32_t* assignment,
+                           double* inertia_out);
+/* modularity (evaluation.cpp:460-483) of a clustering of the context's graph */
+int32_t f2v_modularity(f2v_ctx* ctx, int32_t k, const int32_t* assignment, double* q_out);
+/* best_modularity_sweep (evaluation.cpp:485-497): k in [2, min(kmax, n)] */
+int32_t f2v_best_modularity_sweep(f2v_ctx* ctx, uint64_t* rng_state, int32_t kmax,
+                                  int32_t* k_out, double* q_out);
+
+/* LogRegConfig (evaluation.hpp:46-50) */
+typedef struct {
+  double lr;     /* 0.1 */
+  int32_t iters; /* 500 */
+  double l2;     /* 1e-4 */
+} f2v_logreg_config;
+/* fit_logreg (evaluation.cpp:93-121): features f32[rows * cols] row-major (host),
+ * targets 0/1, weights_out f64[cols + 1] (bias last) */
+int32_t f2v_fit_logreg(f2v_ctx* ctx, const float* features, uint64_t rows, uint32_t cols,
+                       const int32_t* targets, f2v_logreg_config cfg, double* weights_out);
+/* logreg_loss (evaluation.cpp:139-153) */
+int32_t f2v_logreg_loss(f2v_ctx* ctx, const double* weights, const float* features,
+                        uint64_t rows, uint32_t cols, const int32_t* targets, double l2,
+                        double* loss_out);
+/* build_link_dataset (evaluation.cpp:36-85), host: pairs as u32 triples
+ * (u, v, is_edge); *train_out / *test_out allocated by the library (f2v_free) */
+int32_t f2v_build_link_dataset(uint32_t n, const uint64_t* row_offsets,
+                               const uint32_t* col_indices, uint64_t* rng_state,
+                               uint32_t** train_out, uint64_t* ntrain_out, uint32_t** test_out,
+                               uint64_t* ntest_out);
+/* link_prediction_accuracy (evaluation.cpp:155-173) over the context's embedding:
+ * Hadamard features, fit on train, accuracy on test; weights_out nullable */
+int32_t f2v_link_prediction_accuracy(f2v_ctx* ctx, const uint32_t* train, uint64_t ntrain,
+                                     const uint32_t* test, uint64_t ntest, f2v_logreg_config cfg,
+                                     double* accuracy_out, double* weights_out);
+/* node_classification (evaluation.cpp:217-321): labels as a CSR over vertices
+ * (label_offsets u64[n + 1], label_ids sorted and unique per vertex -- what
+ * load_labels produces); one-vs-rest fits run as one batch on the device */
+int32_t f2v_node_classification(f2v_ctx* ctx, const uint64_t* label_offsets,
+                                const int32_t* label_ids, int32_t num_classes,
+                                double train_fraction, uint64_t* rng_state,
+                                f2v_logreg_config cfg, double* micro_f1_out,
+                                double* macro_f1_out);
 
 #ifdef __cplusplus
 }

@@ -55,7 +55,7 @@ void DeviceBuf::release() {
 
 static thread_local std::string g_global_err;
 
-static int32_t guard(Ctx* c, const std::function<void()>& fn) {
+int32_t guard(Ctx* c, const std::function<void()>& fn) {
   try {
     fn();
     if (c) c->err.clear();
@@ -371,10 +371,6 @@ static void train_allgather_impl(Ctx& c, const f2v_train_config& cfg, double* lo
 }  // namespace f2v
 
 using namespace f2v;
-
-struct f2v_ctx {
-  Ctx c;
-};
 
 extern "C" {
 

@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(kWarps * 32, MINB) epoch_kernel(EpochArgs a) {
 template <int KIND, int K, bool VEC, bool MON, bool FAST, int MINB, bool EMUL = false>
 void launch_one(Ctx& c, const EpochArgs& a) {
   auto kern = epoch_kernel<KIND, K, VEC, MON, FAST, MINB, EMUL>;
-  const size_t dsmem = uses_ring<K, VEC, FAST>() ? size_t(kWarps) * kRingWarpBytes : 0;
+  const size_t dsmem = size_t(kWarps) * warp_smem_bytes<K, VEC, FAST>();
   if (dsmem) F2V_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            int(dsmem)));
   if (c.dry_launch) {  // load the function only (CUDA lazy loading) -- no launch
@@ -613,7 +613,7 @@ void launch_one(Ctx& c, const EpochArgs& a) {
 // ms at 2 (128); with the TMA row ring (F2V_ROW_TMA_EXACT) 2 is better: 56.3
 // ms against 66.5 ms at 3 with one ring stage (the ring's shared memory
 // costs resident L1)
-#define F2V_EXACT_MINB (F2V_ROW_TMA_EXACT ? 2 : 3)
+#define F2V_EXACT_MINB ((F2V_EXACT_V3 || F2V_ROW_TMA_EXACT) ? 2 : 3)
 #endif
 
 #ifndef F2V_FAST_MINB_HI

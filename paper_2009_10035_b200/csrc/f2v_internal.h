@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -211,4 +212,31 @@ void k_epoch_negatives(Ctx& c, uint32_t s, uint32_t epoch, uint64_t seed, int sa
 AgResult k_allgather_epoch(Ctx& c, uint32_t s, float eta, const ForceParams& fp, bool monitor,
                            bool fast);
 
+
+// the C-ABI wrapper pattern: run fn, map f2v::Error to its code and message
+int32_t guard(Ctx* c, const std::function<void()>& fn);
+
+// evaluation after training (f2v_eval.cu; evaluation.cpp in the reference)
+namespace ev {
+double kmeans(Ctx& c, const float* z, uint64_t n, uint32_t d, int k, uint64_t& rng, int restarts,
+              int max_iters, int32_t* assign_host);
+double kmeans_inertia(Ctx& c, const float* z, uint64_t n, uint32_t d, int k,
+                      const int32_t* assign_host);
+double modularity(Ctx& c, int k, const int32_t* assign_host);
+void fit_logreg(Ctx& c, const float* x_host, uint64_t n, uint32_t d, const int32_t* targets,
+                double lr, int iters, double l2, double* weights_out);
+double logreg_loss(Ctx& c, const double* weights, const float* x_host, uint64_t n, uint32_t d,
+                   const int32_t* targets, double l2);
+double link_accuracy(Ctx& c, const float* z, uint32_t d, const uint32_t* train_pairs,
+                     uint64_t ntrain, const uint32_t* test_pairs, uint64_t ntest, double lr,
+                     int iters, double l2, double* weights_out);
+void one_vs_rest(Ctx& c, const float* z, uint32_t d, const uint32_t* train_ids, uint64_t ntrain,
+                 const uint32_t* test_ids, uint64_t ntest, uint32_t M, const uint8_t* tgt,
+                 double lr, int iters, double l2, double* weights_out, double* prob_out);
+}  // namespace ev
+
 }  // namespace f2v
+
+struct f2v_ctx {
+  f2v::Ctx c;
+};

@@ -212,7 +212,7 @@ __global__ void ag_scatter_kernel(AgArgs a) {
 template <int KIND, int K, bool VEC, bool FAST>
 void launch_ag_step(const AgArgs& a, bool mon, cudaStream_t st) {
   const uint32_t blocks = std::max(1u, (a.cnt * 32 + 255) / 256);
-  const size_t dsmem = uses_ring<K, VEC, FAST>() ? 8 * kRingWarpBytes : 0;
+  const size_t dsmem = 8 * size_t(warp_smem_bytes<K, VEC, FAST>());
   auto k1 = ag_step_kernel<KIND, K, VEC, true, FAST>;
   auto k0 = ag_step_kernel<KIND, K, VEC, false, FAST>;
   if (dsmem) {

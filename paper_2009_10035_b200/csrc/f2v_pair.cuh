@@ -187,11 +187,34 @@ constexpr int kRingStages = F2V_RING_STAGES;
 constexpr uint32_t kRowBytes = 512;  // d = 128 rows (the ring serves the VEC K = 4 layouts)
 constexpr uint32_t kRingWarpBytes = 128 + kRingStages * 8 * kRowBytes;  // barriers + slots
 
-// the row layouts that stream through the ring (kernels launch with its
-// dynamic shared memory and initialise it)
+// EXACT d = 128 (rows_exact128): per warp, kXStages x 8 row slots filled by
+// cp.async, the transposed-reduction scratch (8 pairs x 32 lane partials,
+// row stride kXRedStride doubles: conflict-free 16-byte reads) and the 8
+// pairs' coefficients.
+#ifndef F2V_EXACT_V3
+#define F2V_EXACT_V3 1
+#endif
+#ifndef F2V_XSTAGES
+#define F2V_XSTAGES 1
+#endif
+constexpr uint32_t kXStages = F2V_XSTAGES;
+constexpr uint32_t kXRedStride = 40;
+constexpr uint32_t kXRedOff = kXStages * 8 * kRowBytes;
+constexpr uint32_t kXCoefOff = kXRedOff + 8 * kXRedStride * 8;
+constexpr uint32_t kXWarpBytes = kXCoefOff + 384;
+
+// dynamic shared memory per warp of a kernel instantiated for this row layout
+// (0 = none); kernels launch with kWarps x this and call ring_init
 template <int K, bool VEC, bool FAST>
-__host__ __device__ constexpr bool uses_ring() {
-  return K == 4 && VEC && (FAST ? F2V_ROW_TMA_FAST != 0 : F2V_ROW_TMA_EXACT != 0);
+__host__ __device__ constexpr uint32_t warp_smem_bytes() {
+  if (!(K == 4 && VEC)) return 0;
+  if (FAST) return F2V_ROW_TMA_FAST ? kRingWarpBytes : 0;
+  if (F2V_EXACT_V3) return kXWarpBytes;
+  return F2V_ROW_TMA_EXACT ? kRingWarpBytes : 0;
+}
+template <int K, bool VEC, bool FAST>
+__host__ __device__ constexpr bool uses_ring() {  // the TMA ring (mbarriers to initialise)
+  return warp_smem_bytes<K, VEC, FAST>() == kRingWarpBytes;
 }
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -201,6 +224,9 @@ extern __shared__ __align__(128) uint8_t f2v_dsmem[];
 // this warp's ring: [0, 8 S) mbarriers, [64] phase bits, slots from 128
 __device__ __forceinline__ uint8_t* ring_base() {
   return f2v_dsmem + (threadIdx.x >> 5) * kRingWarpBytes;
+}
+__device__ __forceinline__ uint8_t* xstage_base() {
+  return f2v_dsmem + (threadIdx.x >> 5) * kXWarpBytes;
 }
 __device__ __forceinline__ void ring_init(int lane) {
   uint8_t* b = ring_base();
@@ -726,6 +752,212 @@ __device__ __forceinline__ double reduce8d(double (&p)[8], int lane) {
   return p[0];
 }
 
+// ------------------------------------------------- EXACT, d = 128 (round 2)
+// The same arithmetic as rows_exact8 (fp64 in the reference's operation
+// order, per-lane partial dots, a transposed reduction so each pair's force
+// term is evaluated once per 4-lane group), restructured after the ncu
+// capture profiles/r2_c3_exact_v3 (108 warp instructions per pair, 120 register
+// moves and 56 sentinel compares per 8-row block, a warp-serialised 9-
+// instruction loop per TMA row copy):
+//  * the next block's 8 rows stream into shared memory with cp.async.cg (one
+//    16-byte copy per lane per row, L2-coherent like ld.cg, no uniform-register
+//    hand-off), waited on per block;
+//  * no per-row predication: rows past the end of the call repeat the last
+//    valid row with a zero coefficient (acc + 0.0 == acc: an accumulator that
+//    starts at +0.0 never becomes -0.0 under round-to-nearest);
+//  * the sentinel test is the dot itself: a row that still holds the sentinel
+//    NaN gives a NaN reduction, and only then are the block's Znew rows polled
+//    and the dots recomputed (a genuine NaN polls once and goes on);
+//  * the 8 x 32 lane partials are transposed through shared memory (8 stores,
+//    4 16-byte loads, 7 adds, two shuffle rounds) instead of a select-and-
+//    shuffle network, and the 8 pairs' coefficients go back through shared
+//    memory as broadcast loads instead of 16+ shuffles.
+struct XCoef {
+  double c[8], sc[8], tr[8], inv[8];
+  int fl[8];
+};
+static_assert(sizeof(XCoef) <= 384, "coefficient block");
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// sum over the 32 lanes of partial number pi = lane >> 2, on every lane:
+// 8 x 32 partials through shared memory (conflict-free), then two rounds
+__device__ __forceinline__ double reduce8x(double (&part)[8], double* red, int lane) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[i * kXRedStride + lane] = part[i];
+  __syncwarp();
+  const double2* rp =
+      reinterpret_cast<const double2*>(red + (lane >> 2) * kXRedStride + (lane & 3) * 2);
+  double2 t[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) t[q] = rp[q * 4];
+  double s = __dadd_rn(__dadd_rn(__dadd_rn(t[0].x, t[0].y), __dadd_rn(t[1].x, t[1].y)),
+                       __dadd_rn(__dadd_rn(t[2].x, t[2].y), __dadd_rn(t[3].x, t[3].y)));
+  s = __dadd_rn(s, __shfl_xor_sync(kFull, s, 1));
+  s = __dadd_rn(s, __shfl_xor_sync(kFull, s, 2));
+  return s;
+}
+
+template <int KIND, bool MON, bool ATT>
+__device__ __forceinline__ void rows_exact128(const ForceParams& fp, uint32_t packed, int cnt,
+                                              int lane, const float* __restrict__ zold,
+                                              const float* __restrict__ znew,
+                                              const float (&zu)[4], double (&acc_io)[4],
+                                              double& lsum_io) {
+  static_assert(KIND >= 0, "compiled per force kind");
+  constexpr int K = 4;
+  constexpr uint32_t d = 128;
+  using L = Lay<K, true>;
+  constexpr bool SIG = KIND == F2V_SIGMOID;
+  constexpr bool SCALED = !ATT;  // repulsive kinds may be clamped (a second multiply)
+  if (cnt <= 0) return;
+  uint8_t* base = xstage_base();
+  const uint32_t slots = smem_addr(base) + 16 * lane;
+  const float4* slotp = reinterpret_cast<const float4*>(base) + lane;
+  double* red = reinterpret_cast<double*>(base + kXRedOff);
+  XCoef* cf = reinterpret_cast<XCoef*>(base + kXCoefOff);
+  const int pi = lane >> 2;
+  double uu[K], acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    uu[k] = zu[k];
+    acc[k] = acc_io[k];
+  }
+  double lsum = lsum_io;
+  // this lane's 16 bytes of the row whose id lane min(lane, cnt - 1) holds
+  const uint32_t pkc = __shfl_sync(kFull, packed, min(lane, cnt - 1));
+  const char* mine = reinterpret_cast<const char*>(((pkc & kNewBit) ? znew : zold) +
+                                                   size_t(pkc & ~kNewBit) * d);
+  auto issue = [&](int k0, int st) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const char* src = reinterpret_cast<const char*>(
+          __shfl_sync(kFull, reinterpret_cast<unsigned long long>(mine), (k0 + i) & 31));
+      cp_async16(slots + (st * 8 + i) * kRowBytes, src + 16 * lane);
+    }
+    cp_async_commit();
+  };
+  const int nblk = (cnt + 7) >> 3;
+#pragma unroll
+  for (int b = 0; b < int(kXStages); ++b)
+    if (b < nblk) issue(8 * b, b);
+  for (int b = 0; b < nblk; ++b) {
+    const int k0 = 8 * b, st = kXStages == 1 ? 0 : b % int(kXStages);
+    if (kXStages == 1 || b + int(kXStages) > nblk) cp_async_wait<0>();
+    else cp_async_wait<int(kXStages) - 1>();
+    float v[8][K];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 t = slotp[(st * 8 + i) * (kRowBytes / 16)];
+      v[i][0] = t.x; v[i][1] = t.y; v[i][2] = t.z; v[i][3] = t.w;
+    }
+    if (b + int(kXStages) < nblk) issue(k0 + 8 * int(kXStages), st);
+    double w[8][K], red_p, nrm_p = 0.0;
+    bool polled = false;
+    for (;;) {
+      // per-lane fp64 partial dot / distance of the 8 pairs.  Sigmoid: the
+      // products of two floats are exact in fp64, so fma(u, o, s) rounds exactly
+      // like the reference's separate multiply and add (force_kernels.cpp:30-34).
+      double part[8], nrm[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        double s = 0.0, q = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double o = double(v[i][k]);
+          if (SIG) {
+            w[i][k] = o;
+            s = __fma_rn(uu[k], o, s);
+            if (!ATT) q = __fma_rn(o, o, q);
+          } else {  // distance(): diff * diff may be inexact -> separate roundings
+            w[i][k] = __dsub_rn(uu[k], o);
+            s = __dadd_rn(s, __dmul_rn(w[i][k], w[i][k]));
+          }
+        }
+        part[i] = s;
+        nrm[i] = q;
+      }
+      red_p = reduce8x(part, red, lane);
+      if (SIG && !ATT) {
+        __syncwarp();
+        nrm_p = reduce8x(nrm, red, lane);
+      }
+      // a Znew row not yet final still holds the sentinel NaN -> NaN here
+      if (polled || !__any_sync(kFull, red_p != red_p)) break;
+      polled = true;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t pk = __shfl_sync(kFull, packed, min(k0 + i, cnt - 1));
+        if (pk & kNewBit) L::poll(znew + size_t(pk & ~kNewBit) * d, lane, d, v[i], fp.stall);
+      }
+      __syncwarp();
+    }
+    Term t = pair_term<MON>(KIND, fp, ATT, red_p, nrm_p);  // pair pi, once per 4-lane group
+    const bool valid = k0 + pi < cnt;
+    if (MON && (lane & 3) == 0 && valid) lsum = __dadd_rn(lsum, t.loss);
+    if ((lane & 3) == 0) {  // rows past the end: a zero coefficient on a finite row
+      cf->c[pi] = valid ? t.coef : 0.0;
+      if (SCALED) cf->sc[pi] = t.clamped ? t.scale : 1.0;
+      if (!SIG) {
+        cf->tr[pi] = valid ? t.r : 1.0;
+        cf->inv[pi] = valid ? t.inv : 1.0;
+      }
+      if (SCALED || !SIG)
+        cf->fl[pi] = valid ? ((t.fallback ? 1 : 0) | (t.clamped ? 2 : 0)) : 0;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double c = cf->c[i];
+      const int f = (SCALED || !SIG) ? cf->fl[i] : 0;
+      if (SIG) {  // out_j = c z_j (x scale): scale_into + clamp_magnitude
+        if (SCALED && (f & 2)) {
+          const double si = cf->sc[i];
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            acc[k] = __dadd_rn(acc[k], __dmul_rn(__dmul_rn(c, w[i][k]), si));
+        } else {
+#pragma unroll
+          for (int k = 0; k < K; ++k) acc[k] = __dadd_rn(acc[k], __dmul_rn(c, w[i][k]));
+        }
+      } else {
+        const double si = SCALED ? cf->sc[i] : 1.0;
+        if (f & 1) {  // coincident: out = (c, 0, ..., 0) (scaled_unit_diff)
+          if (lane == 0) {
+            double o = c;
+            if (f & 2) o = __dmul_rn(o, si);
+            acc[0] = __dadd_rn(acc[0], o);
+          }
+          const double zero = (f & 2) ? __dmul_rn(0.0, si) : 0.0;
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            if (lane != 0 || k != 0) acc[k] = __dadd_rn(acc[k], zero);
+        } else {  // out_j = (c (u_j - o_j)) / t (force_kernels.cpp:63-64)
+          const double tr = cf->tr[i], inv = cf->inv[i];
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            double o = div_by(__dmul_rn(c, w[i][k]), tr, inv);
+            if (SCALED && (f & 2)) o = __dmul_rn(o, si);
+            acc[k] = __dadd_rn(acc[k], o);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc_io[k] = acc[k];
+  lsum_io = lsum;
+}
+
 template <int KIND, int K, bool MON, bool ATT>
 __device__ __forceinline__ void rows_exact8(const ForceParams& fp, uint32_t packed, int cnt,
                                             int lane, uint32_t d, const float* __restrict__ zold,
@@ -997,6 +1229,8 @@ struct Rows {
       rows_lowd<KIND, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else if constexpr (FAST)
       rows_fast<KIND, K, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
+    else if constexpr (VEC && KIND >= 0 && K == 4 && F2V_EXACT_V3 != 0)
+      rows_exact128<KIND, MON, ATT>(fp, packed, cnt, lane, zold, znew, zu, acc, lsum);
     else if constexpr (VEC && KIND >= 0)
       rows_exact8<KIND, K, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else
