@@ -14,6 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <fstream>
+#include <iostream>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -27,6 +28,9 @@
 using namespace force2vec;
 
 namespace {
+// libstdc++ is linked statically into libf2vref.so: its stream/locale state is
+// initialised only if some translation unit constructs ios_base::Init
+std::ios_base::Init g_ios_init;
 thread_local std::string g_err;
 
 int classify(const std::exception& e) {

@@ -93,6 +93,10 @@ class _Counters(C.Structure):
     _fields_ = [("attractive_evals", C.c_uint64), ("repulsive_evals", C.c_uint64)]
 
 
+class _LogRegConfig(C.Structure):
+    _fields_ = [("lr", C.c_double), ("iters", C.c_int32), ("l2", C.c_double)]
+
+
 class _Failure(C.Structure):
     _fields_ = [("epoch", C.c_uint32), ("batch", C.c_uint64), ("vertex", C.c_uint32)]
 
@@ -101,6 +105,7 @@ _u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
 _u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
 _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+_i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
 _vp = C.c_void_p
 _i32 = C.c_int32
 
@@ -166,6 +171,29 @@ SYMBOLS = {
                                           C.POINTER(_Failure)]),
     "f2v_get_rows": (_i32, [_vp, _u32p, C.c_uint32, _f32p]),
     "f2v_set_rows": (_i32, [_vp, _u32p, C.c_uint32, _f32p]),
+    # after training: embedding text I/O and evaluation (evaluation.py)
+    "f2v_write_embedding": (_i32, [C.c_char_p, _f32p, C.c_uint32, C.c_uint32]),
+    "f2v_read_embedding": (_i32, [C.c_char_p, C.POINTER(C.POINTER(C.c_float)),
+                                  C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
+    "f2v_write_layout_tsv": (_i32, [C.c_char_p, _f32p, C.c_uint32, C.c_uint32, _vp]),
+    "f2v_rng_state": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+    "f2v_kmeans": (_i32, [_vp, _i32, C.POINTER(C.c_uint64), _i32, _i32, _i32p,
+                          C.POINTER(C.c_double)]),
+    "f2v_kmeans_inertia": (_i32, [_vp, _i32, _i32p, C.POINTER(C.c_double)]),
+    "f2v_modularity": (_i32, [_vp, _i32, _i32p, C.POINTER(C.c_double)]),
+    "f2v_best_modularity_sweep": (_i32, [_vp, C.POINTER(C.c_uint64), _i32, C.POINTER(_i32),
+                                         C.POINTER(C.c_double)]),
+    "f2v_fit_logreg": (_i32, [_vp, _f32p, C.c_uint64, C.c_uint32, _i32p, _LogRegConfig, _f64p]),
+    "f2v_logreg_loss": (_i32, [_vp, _f64p, _f32p, C.c_uint64, C.c_uint32, _i32p, C.c_double,
+                               C.POINTER(C.c_double)]),
+    "f2v_build_link_dataset": (_i32, [C.c_uint32, _u64p, _u32p, C.POINTER(C.c_uint64),
+                                      C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_uint64),
+                                      C.POINTER(C.POINTER(C.c_uint32)), C.POINTER(C.c_uint64)]),
+    "f2v_link_prediction_accuracy": (_i32, [_vp, _u32p, C.c_uint64, _u32p, C.c_uint64,
+                                            _LogRegConfig, C.POINTER(C.c_double), _vp]),
+    "f2v_node_classification": (_i32, [_vp, _u64p, _i32p, _i32, C.c_double,
+                                       C.POINTER(C.c_uint64), _LogRegConfig,
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 

@@ -155,11 +155,15 @@ __device__ __forceinline__ float* znew_of(const EpochArgs& a, uint32_t u) {
 
 // Per-warp FIFO of packed row ids (bit 31 = Znew) in shared memory; rows
 // are accumulated 32 at a time in push order (= the deterministic pair order).
-#ifndef F2V_E_PREFETCH
 // E items: the next groups' column ids / states in flight while this group's
-// rows are reduced.  Measured slower (same box: C3 FAST 28.9 -> 29.5 ms, C3
-// EXACT 50.2 -> 52.1 ms: the extra registers live across the row calls), off.
-#define F2V_E_PREFETCH 0
+// rows are reduced (the col -> state -> row chain is three dependent loads per
+// arc).  Same-box A/B: EXACT C3 kernel 36.1 -> 35.2 ms (on); FAST C3 28.9 ->
+// 29.5 ms (off: its 80-register build spills the prefetched words).
+#ifndef F2V_E_PREFETCH_EXACT
+#define F2V_E_PREFETCH_EXACT 1
+#endif
+#ifndef F2V_E_PREFETCH_FAST
+#define F2V_E_PREFETCH_FAST 0
 #endif
 
 #ifndef F2V_INLINE_E
@@ -297,23 +301,27 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   // are gathered and reduced, group i+1's states and group i+2's column ids
   // are already in flight (the col -> state -> row chain is three dependent
   // loads per arc).
-#if F2V_E_PREFETCH
-  uint32_t v_cur = e0 + lane < e1 ? __ldg(a.col + e0 + lane) : 0u;  // this group's ids
-  uint32_t v_nx = e0 + 32 + lane < e1 ? __ldg(a.col + e0 + 32 + lane) : 0u;  // the next's
-  uint32_t st_cur = e0 + lane < e1 ? ld_relaxed(a.state + v_cur) : 0u;  // this group's states
-#endif
+  constexpr bool PRE = FAST ? F2V_E_PREFETCH_FAST != 0 : F2V_E_PREFETCH_EXACT != 0;
+  uint32_t v_cur = 0, v_nx = 0, st_cur = 0;
+  if constexpr (PRE) {
+    v_cur = e0 + lane < e1 ? __ldg(a.col + e0 + lane) : 0u;            // this group's ids
+    v_nx = e0 + 32 + lane < e1 ? __ldg(a.col + e0 + 32 + lane) : 0u;  // the next's
+    st_cur = e0 + lane < e1 ? ld_relaxed(a.state + v_cur) : 0u;       // this group's states
+  }
   for (uint64_t e = e0; e < e1; e += 32) {
     const int cnt = int(umin64(32, e1 - e));
-#if F2V_E_PREFETCH
-    const uint32_t v = v_cur, st = st_cur;
-    // issue the next group's states and the group after's column ids
-    st_cur = e + 32 + lane < e1 ? ld_relaxed(a.state + v_nx) : 0u;
-    v_cur = v_nx;
-    v_nx = e + 64 + lane < e1 ? __ldg(a.col + e + 64 + lane) : 0u;
-#else
-    const uint32_t v = lane < cnt ? a.col[e + lane] : 0u;
-    const uint32_t st = lane < cnt ? ld_relaxed(a.state + v) : 0u;
-#endif
+    uint32_t v, st;
+    if constexpr (PRE) {
+      v = v_cur;
+      st = st_cur;
+      // issue the next group's states and the group after's column ids
+      st_cur = e + 32 + lane < e1 ? ld_relaxed(a.state + v_nx) : 0u;
+      v_cur = v_nx;
+      v_nx = e + 64 + lane < e1 ? __ldg(a.col + e + 64 + lane) : 0u;
+    } else {
+      v = lane < cnt ? a.col[e + lane] : 0u;
+      st = lane < cnt ? ld_relaxed(a.state + v) : 0u;
+    }
     uint32_t pk = 0;
     bool use = false, win = false;
     if (lane < cnt) {
