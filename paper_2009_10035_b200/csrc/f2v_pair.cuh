@@ -772,6 +772,10 @@ __device__ __forceinline__ double reduce8d(double (&p)[8], int lane) {
 //    4 16-byte loads, 7 adds, two shuffle rounds) instead of a select-and-
 //    shuffle network, and the 8 pairs' coefficients go back through shared
 //    memory as broadcast loads instead of 16+ shuffles.
+// Measured and rejected (same-box A/B, C3 kernel): two cp.async stages 36.1 ->
+// 40.8 ms (the second stage's shared memory costs L1); 3 CTAs/SM at 80
+// registers 53 ms (spills); issuing the first block of the row queue's NEXT
+// call during this call's last block (cross-call prefetch) 35.3 -> 42.1 ms.
 struct XCoef {
   double c[8], sc[8], tr[8], inv[8];
   int fl[8];
