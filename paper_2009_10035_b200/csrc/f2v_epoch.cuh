@@ -157,13 +157,14 @@ __device__ __forceinline__ float* znew_of(const EpochArgs& a, uint32_t u) {
 // are accumulated 32 at a time in push order (= the deterministic pair order).
 // E items: the next groups' column ids / states in flight while this group's
 // rows are reduced (the col -> state -> row chain is three dependent loads per
-// arc).  Same-box A/B: EXACT C3 kernel 36.1 -> 35.2 ms (on); FAST C3 28.9 ->
-// 29.5 ms (off: its 80-register build spills the prefetched words).
+// arc).  Same-box A/B, C3 kernel: EXACT 36.1 -> 35.2 ms; FAST 27.3 -> 25.4 ms
+// with the round-2 row function (it was a loss, 28.9 -> 29.5 ms, while the old
+// 80-register row function spilled the prefetched words); C2 neutral.
 #ifndef F2V_E_PREFETCH_EXACT
 #define F2V_E_PREFETCH_EXACT 1
 #endif
 #ifndef F2V_E_PREFETCH_FAST
-#define F2V_E_PREFETCH_FAST 0
+#define F2V_E_PREFETCH_FAST 1
 #endif
 
 #ifndef F2V_INLINE_E
