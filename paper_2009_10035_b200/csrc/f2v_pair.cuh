@@ -194,6 +194,7 @@ constexpr uint32_t kRingWarpBytes = 128 + kRingStages * 8 * kRowBytes;  // barri
 #ifndef F2V_EXACT_V3
 #define F2V_EXACT_V3 1
 #endif
+
 #ifndef F2V_XSTAGES
 #define F2V_XSTAGES 1
 #endif
@@ -227,6 +228,16 @@ __device__ __forceinline__ uint8_t* ring_base() {
 }
 __device__ __forceinline__ uint8_t* xstage_base() {
   return f2v_dsmem + (threadIdx.x >> 5) * kXWarpBytes;
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void ring_init(int lane) {
   uint8_t* b = ring_base();
@@ -635,9 +646,19 @@ __device__ __forceinline__ void fast_block(const ForceParams& fp, int k0, int cn
 //  * the sentinel test is the dot: a row that still holds the sentinel NaN
 //    gives a NaN reduction, and only then are the block's Znew rows polled
 //    through L2 and the dots recomputed.
+// Measured and rejected on top of it (same-box A/B, C3 / C2 kernel ms; the
+// default is 25.4 / 7.2): the next block staged in shared memory by cp.async.ca
+// 25.3 / 7.7; the next block's gathers issued into a second register block
+// before this block's math 29.0 / 11.8; 4 CTAs/SM at 64 registers 34.0 / 13.8;
+// forcing the 3-CTA build 28.0 / 11.1 (the occupancy autotune picks 2 CTAs/SM on
+// both graphs).  Every variant that puts more gathers in flight per SM loses:
+// with power-law degrees L1 serves a large share of the row reads, and on a
+// near-regular graph of the same size (tools/skew_probe.py) the kernel is
+// slower (30.1 ms), not faster.
 #ifndef F2V_FAST_V3
 #define F2V_FAST_V3 1
 #endif
+
 template <int KIND, bool MON, bool ATT>
 __device__ __forceinline__ void rows_fast128(const ForceParams& fp, uint32_t packed, int cnt,
                                              int lane, const float* __restrict__ zold,
@@ -653,8 +674,7 @@ __device__ __forceinline__ void rows_fast128(const ForceParams& fp, uint32_t pac
   const uint32_t pkc = __shfl_sync(kFull, packed, min(lane, cnt - 1));
   const char* mine = reinterpret_cast<const char*>(((pkc & kNewBit) ? znew : zold) +
                                                    size_t(pkc & ~kNewBit) * d);
-  for (int k0 = 0; k0 < cnt; k0 += 8) {
-    float w[8][K];
+  auto load_block = [&](int k0, float (&w)[8][K]) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const char* src = reinterpret_cast<const char*>(
@@ -662,6 +682,8 @@ __device__ __forceinline__ void rows_fast128(const ForceParams& fp, uint32_t pac
       const float4 t = *reinterpret_cast<const float4*>(src + 16 * lane);
       w[i][0] = t.x; w[i][1] = t.y; w[i][2] = t.z; w[i][3] = t.w;
     }
+  };
+  auto compute_block = [&](int k0, float (&w)[8][K]) {
     float red, nr = 0.f;
     bool polled = false;
     for (;;) {
@@ -718,6 +740,11 @@ __device__ __forceinline__ void rows_fast128(const ForceParams& fp, uint32_t pac
     }
 #pragma unroll
     for (int k = 0; k < K; ++k) acc[k] = __dadd_rn(acc[k], double(a32[k]));
+  };
+  for (int k0 = 0; k0 < cnt; k0 += 8) {
+    float w[8][K];
+    load_block(k0, w);
+    compute_block(k0, w);
   }
 }
 
@@ -882,16 +909,6 @@ struct XCoef {
 };
 static_assert(sizeof(XCoef) <= 384, "coefficient block");
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() {
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 // sum over the 32 lanes of partial number pi = lane >> 2, on every lane:
 // 8 x 32 partials through shared memory (conflict-free), then two rounds
