@@ -229,8 +229,18 @@ __device__ __forceinline__ uint8_t* ring_base() {
 __device__ __forceinline__ uint8_t* xstage_base() {
   return f2v_dsmem + (threadIdx.x >> 5) * kXWarpBytes;
 }
+#ifndef F2V_EXACT_LOAD
+// rows_exact128 row fetch: 0 cp.async.cg staging (L2; the default), 1 cp.async.ca (through
+// L1), 2 direct register loads.  Same-box A/B, C3 / C2 kernel ms: 35.0 / 16.9, 37.4 / 17.4,
+// 39.6 / 17.1.
+#define F2V_EXACT_LOAD 0
+#endif
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+#if F2V_EXACT_LOAD == 1
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#else
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -968,20 +978,32 @@ __device__ __forceinline__ void rows_exact128(const ForceParams& fp, uint32_t pa
     cp_async_commit();
   };
   const int nblk = (cnt + 7) >> 3;
+#if F2V_EXACT_LOAD != 2
 #pragma unroll
   for (int b = 0; b < int(kXStages); ++b)
     if (b < nblk) issue(8 * b, b);
+#endif
   for (int b = 0; b < nblk; ++b) {
     const int k0 = 8 * b, st = kXStages == 1 ? 0 : b % int(kXStages);
+    float v[8][K];
+#if F2V_EXACT_LOAD == 2
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const char* src = reinterpret_cast<const char*>(
+          __shfl_sync(kFull, reinterpret_cast<unsigned long long>(mine), (k0 + i) & 31));
+      const float4 t = *reinterpret_cast<const float4*>(src + 16 * lane);
+      v[i][0] = t.x; v[i][1] = t.y; v[i][2] = t.z; v[i][3] = t.w;
+    }
+#else
     if (kXStages == 1 || b + int(kXStages) > nblk) cp_async_wait<0>();
     else cp_async_wait<int(kXStages) - 1>();
-    float v[8][K];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const float4 t = slotp[(st * 8 + i) * (kRowBytes / 16)];
       v[i][0] = t.x; v[i][1] = t.y; v[i][2] = t.z; v[i][3] = t.w;
     }
     if (b + int(kXStages) < nblk) issue(k0 + 8 * int(kXStages), st);
+#endif
     double w[8][K], red_p, nrm_p = 0.0;
     bool polled = false;
     for (;;) {
