@@ -1,8 +1,2 @@
-python -m pytest tests -m gpu -x -q > gpurun_out/r2_gputests_v6.log 2>&1; tail -3 gpurun_out/r2_gputests_v6.log
-python bench.py > gpurun_out/r2_bench_default_v6.json 2> gpurun_out/r2_bench_default_v6.err; tail -c 300 gpurun_out/r2_bench_default_v6.json
-python bench.py --impl reference > gpurun_out/r2_bench_reference_v6.json 2> gpurun_out/r2_bench_reference_v6.err; tail -c 300 gpurun_out/r2_bench_reference_v6.json
-for c in c1 c2 c4; do python bench.py --config $c --no-cpu-baseline > gpurun_out/r2_bench_${c}_v6.json 2> gpurun_out/r2_bench_${c}_v6.err; done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:epoch_kernel --launch-skip 3 --launch-count 1 -o gpurun_out/r2_c3_exact_v6 python bench.py --precision exact --steps 1 --warmup 3 --no-cpu-baseline --no-fast --no-per-step > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:epoch_kernel --launch-skip 5 --launch-count 1 -o gpurun_out/r2_c3_fast_v6 python bench.py --precision fast --steps 1 --warmup 3 --no-cpu-baseline --no-per-step > /dev/null 2>&1
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r2_c3_launches_v6.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-fast --no-per-step > /dev/null 2>&1
-ls gpurun_out | grep v6
+python tools/eval_timing.py > gpurun_out/eval_timing.log 2>&1; cat gpurun_out/eval_timing.log
+F2V_RUN_C5=1 timeout 2400 python -m pytest tests/test_gpu_c5.py -x -q -s > gpurun_out/r2_c5_parity_v6.log 2>&1; tail -15 gpurun_out/r2_c5_parity_v6.log
