@@ -367,6 +367,71 @@ __global__ void logreg_step_kernel(const float* __restrict__ x, uint64_t n, uint
   }
 }
 
+// The same step with the rows streamed through shared memory: tiles of R rows
+// (contiguous R x d floats) and their R errors are copied in by cp.async, double
+// buffered, while the previous tile is accumulated -- the per-row cost drops
+// from a global-load latency (~175 ns/row measured) to the dependent fp64 add.
+// Same sums in the same order as logreg_step_kernel.
+__global__ void logreg_step_tiled_kernel(const float* __restrict__ x, uint64_t n, uint32_t d,
+                                         const double* __restrict__ err, double* __restrict__ w,
+                                         double lr, double l2, uint32_t R) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t m = blockIdx.x, j = threadIdx.x;
+  const double* e = err + size_t(m) * n;
+  double* wm = w + size_t(m) * (d + 1);
+  const size_t tile_bytes = size_t(R) * d * sizeof(float);
+  float* tile[2] = {reinterpret_cast<float*>(smem), reinterpret_cast<float*>(smem + tile_bytes)};
+  double* et[2] = {reinterpret_cast<double*>(smem + 2 * tile_bytes),
+                   reinterpret_cast<double*>(smem + 2 * tile_bytes) + R};
+  const uint64_t ntiles = (n + R - 1) / R;
+  auto load = [&](uint64_t t, int b) {
+    const uint64_t r0 = t * R;
+    const uint32_t rows = uint32_t(min(uint64_t(R), n - r0));
+    const size_t bytes = size_t(rows) * d * sizeof(float);
+    const char* src = reinterpret_cast<const char*>(x + r0 * d);
+    if (bytes % 16 == 0) {
+      const uint32_t dst = uint32_t(__cvta_generic_to_shared(tile[b]));
+      for (size_t off = size_t(threadIdx.x) * 16; off < bytes; off += size_t(blockDim.x) * 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + uint32_t(off)),
+                     "l"(src + off)
+                     : "memory");
+    } else {  // a ragged last tile
+      for (size_t q = threadIdx.x; q < size_t(rows) * d; q += blockDim.x)
+        tile[b][q] = x[r0 * d + q];
+    }
+    for (uint32_t r = threadIdx.x; r < rows; r += blockDim.x) et[b][r] = e[r0 + r];
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double g = 0.0;
+  if (ntiles) load(0, 0);
+  for (uint64_t t = 0; t < ntiles; ++t) {
+    const int b = int(t & 1);
+    if (t + 1 < ntiles) {
+      load(t + 1, b ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t rows = uint32_t(min(uint64_t(R), n - t * R));
+    if (j < d) {
+      const float* col = tile[b] + j;
+#pragma unroll 4
+      for (uint32_t r = 0; r < rows; ++r)
+        g = __dadd_rn(g, __dmul_rn(et[b][r], double(col[size_t(r) * d])));
+    } else if (j == d) {
+#pragma unroll 4
+      for (uint32_t r = 0; r < rows; ++r) g = __dadd_rn(g, et[b][r]);
+    }
+    __syncthreads();  // the buffer is refilled two tiles on
+  }
+  const double inv_n = __ddiv_rn(1.0, double(n));
+  if (j < d)
+    wm[j] = __dsub_rn(wm[j], __dmul_rn(lr, __dadd_rn(__dmul_rn(g, inv_n), __dmul_rn(l2, wm[j]))));
+  else if (j == d)
+    wm[d] = __dsub_rn(wm[d], __dmul_rn(__dmul_rn(lr, g), inv_n));
+}
+
 // prob[i * M + m] = p_m(x_i) (test rows; row-major over models for the host ranking)
 __global__ void logreg_prob_kernel(const float* __restrict__ xt, uint64_t n, uint32_t d,
                                    const double* __restrict__ w, uint32_t M,
@@ -658,12 +723,25 @@ static void fit_models(Ctx& c, LogRegWork& w, uint64_t n, uint32_t d, uint32_t M
   F2V_CUDA(cudaMemcpyAsync(w.tgt.p, tgt_host, size_t(M) * n, cudaMemcpyHostToDevice, c.stream));
   F2V_CUDA(cudaMemsetAsync(w.w.p, 0, sizeof(double) * size_t(M) * (d + 1), c.stream));
   const uint32_t tb = std::min<uint32_t>(1024, (d + 1 + 31) / 32 * 32);
+  // rows per shared-memory tile of the tiled step: two tiles + their errors in <= 160 KB
+  uint32_t R = 64;
+  while (R >= 8 && 2 * (size_t(R) * d * sizeof(float) + R * sizeof(double)) > 160 * 1024) R /= 2;
+  const bool tiled = R >= 8 && d + 1 <= 1024;
+  const size_t tsmem = 2 * (size_t(R) * d * sizeof(float) + R * sizeof(double));
+  if (tiled)
+    F2V_CUDA(cudaFuncSetAttribute(logreg_step_tiled_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(tsmem)));
   for (int it = 0; it < iters; ++it) {
     logreg_err_kernel<<<dim3(grid_for(n), M), kTB, 0, c.stream>>>(
         w.xt.as<float>(), n, d, w.w.as<double>(), w.tgt.as<uint8_t>(), w.err.as<double>());
     F2V_LAUNCHED(c.stream, "logreg_err_kernel");
-    logreg_step_kernel<<<M, tb, 0, c.stream>>>(w.x.as<float>(), n, d, w.err.as<double>(),
-                                               w.w.as<double>(), lr, l2);
+    if (tiled)
+      logreg_step_tiled_kernel<<<M, tb, tsmem, c.stream>>>(w.x.as<float>(), n, d,
+                                                           w.err.as<double>(), w.w.as<double>(),
+                                                           lr, l2, R);
+    else
+      logreg_step_kernel<<<M, tb, 0, c.stream>>>(w.x.as<float>(), n, d, w.err.as<double>(),
+                                                 w.w.as<double>(), lr, l2);
     F2V_LAUNCHED(c.stream, "logreg_step_kernel");
     c.launches += 2;
   }
