@@ -208,6 +208,7 @@ constexpr uint32_t kXWarpBytes = kXCoefOff + 384;
 // (0 = none); kernels launch with kWarps x this and call ring_init
 template <int K, bool VEC, bool FAST>
 __host__ __device__ constexpr uint32_t warp_smem_bytes() {
+  if (K == 1 && !VEC && !FAST) return 4 * 32 * 8;  // rows_lowd_exact's transpose block
   if (!(K == 4 && VEC)) return 0;
   if (FAST) return F2V_ROW_TMA_FAST ? kRingWarpBytes : 0;
   if (F2V_EXACT_V3) return kXWarpBytes;
@@ -1358,6 +1359,97 @@ __device__ __forceinline__ void rows_lowd(const ForceParams& fp, uint32_t packed
   if (lane < int(d)) acc1[0] = __dadd_rn(acc1[0], double(mycol));
 }
 
+// ------------------------------------------------------- EXACT low-d
+// d <= kLowD at the reference's arithmetic (config 4 with precision = exact):
+// the generic masked layout would spend a whole warp butterfly on two columns.
+// Here each lane owns one PAIR: its row is one 8/16-byte load, the fp64 dot /
+// distance runs over the columns sequentially -- exactly the reference's
+// order (force_kernels.cpp:30-43), not a tree -- and the fp64 force term is
+// lane-local.  The per-column accumulate has to stay in pair order
+// (trainer.cpp:129-138): the 32 x d contributions are transposed through a
+// 1 KB per-warp shared-memory block and lane c adds column c's in order (pairs
+// past the end contribute +0.0: acc + 0.0 == acc, see rows_exact128).
+constexpr uint32_t kLowdWarpBytes = kLowD * 32 * sizeof(double);
+__device__ __forceinline__ double* lowd_base() {
+  return reinterpret_cast<double*>(f2v_dsmem + (threadIdx.x >> 5) * kLowdWarpBytes);
+}
+
+template <int KIND, bool MON, bool ATT>
+__device__ __forceinline__ void rows_lowd_exact(const ForceParams& fp, uint32_t packed, int cnt,
+                                                int lane, uint32_t d,
+                                                const float* __restrict__ zold,
+                                                const float* __restrict__ znew,
+                                                const float (&zu1)[1], double (&acc1)[1],
+                                                double& lsum) {
+  static_assert(KIND >= 0, "compiled per force kind");
+  constexpr bool SIG = KIND == F2V_SIGMOID;
+  double zu[kLowD];
+#pragma unroll
+  for (int c = 0; c < kLowD; ++c) zu[c] = double(__shfl_sync(kFull, zu1[0], c));  // lane c = column c
+  const bool mine = lane < cnt;
+  const uint32_t pk = packed;
+  const float* row = ((pk & kNewBit) ? znew : zold) + size_t(pk & ~kNewBit) * d;
+  float w[kLowD];
+  auto load = [&]() {
+#pragma unroll
+    for (int c = 0; c < kLowD; ++c)
+      w[c] = (mine && c < int(d)) ? ((pk & kNewBit) ? __ldcg(row + c) : __ldg(row + c)) : 0.0f;
+  };
+  load();
+  auto pending = [&]() {
+    bool b = false;
+#pragma unroll
+    for (int c = 0; c < kLowD; ++c) b |= __float_as_uint(w[c]) == kSentinel;
+    return b && mine && (pk & kNewBit);
+  };
+  uint32_t ns = 32, it = 0;
+  while (__any_sync(kFull, it < kPollLimit && pending())) {
+    __nanosleep(ns);
+    ns = ns < F2V_POLL_MAX_NS ? 2 * ns : ns;
+    if (pending()) load();
+    if (++it == kPollLimit) poll_stalled(fp.stall);
+  }
+  double x[kLowD], red = 0.0, nrm = 0.0;  // x = the other row (sigmoid) or u - other
+#pragma unroll
+  for (int c = 0; c < kLowD; ++c) {
+    const double o = double(w[c]);
+    if (SIG) {
+      x[c] = o;
+      if (c < int(d)) {
+        red = __dadd_rn(red, __dmul_rn(zu[c], o));
+        if (!ATT) nrm = __dadd_rn(nrm, __dmul_rn(o, o));
+      }
+    } else {
+      x[c] = __dsub_rn(zu[c], o);
+      if (c < int(d)) red = __dadd_rn(red, __dmul_rn(x[c], x[c]));
+    }
+  }
+  const Term t = pair_term<MON>(KIND, fp, ATT, red, nrm);
+  if (MON && mine) lsum = __dadd_rn(lsum, t.loss);
+  double* buf = lowd_base();
+#pragma unroll
+  for (int c = 0; c < kLowD; ++c) {
+    double o;
+    if (!t.dist) {
+      o = __dmul_rn(t.coef, x[c]);
+    } else if (t.fallback) {  // coincident: out = (coef, 0, ..., 0) (scaled_unit_diff)
+      o = c == 0 ? t.coef : 0.0;
+    } else {
+      o = div_by(__dmul_rn(t.coef, x[c]), t.r, t.inv);
+    }
+    if (t.clamped) o = __dmul_rn(o, t.scale);
+    buf[c * 32 + lane] = (mine && c < int(d)) ? o : 0.0;
+  }
+  __syncwarp();
+  if (lane < int(d)) {
+    double a = acc1[0];
+    const double* colp = buf + lane * 32;
+    for (int i = 0; i < cnt; ++i) a = __dadd_rn(a, colp[i]);
+    acc1[0] = a;
+  }
+  __syncwarp();
+}
+
 // The row-accumulation policy the epoch kernel is instantiated with.  run is
 // out of line (one copy per (kind, attractive): the kernel is instruction-
 // fetch sensitive); run_inl is the same body inlined at a hot call site.
@@ -1376,6 +1468,13 @@ struct Rows {
       rows_fast<KIND, K, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else if constexpr (VEC && KIND >= 0 && K == 4 && F2V_EXACT_V3 != 0)
       rows_exact128<KIND, MON, ATT>(fp, packed, cnt, lane, zold, znew, zu, acc, lsum);
+    else if constexpr (!VEC && K == 1 && KIND >= 0) {
+      if (d <= uint32_t(kLowD))
+        rows_lowd_exact<KIND, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
+      else
+        rows_exact<KIND, K, VEC, 4, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc,
+                                              lsum);
+    }
     else if constexpr (VEC && KIND >= 0)
       rows_exact8<KIND, K, MON, ATT>(fp, packed, cnt, lane, d, zold, znew, zu, acc, lsum);
     else

@@ -15,6 +15,8 @@ tests also report the fraction of bit-identical floats.
 """
 import os
 
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -272,7 +274,7 @@ def test_config1_epoch_parity(f2v, orc, dev, sampler, precision):
 
 @pytest.mark.parametrize("precision", PRECISIONS)
 @pytest.mark.parametrize("kind", KINDS)
-@pytest.mark.parametrize("d", [2, 16, 64, 100, 128, 256])
+@pytest.mark.parametrize("d", [2, 3, 16, 64, 100, 128, 256])
 def test_epoch_parity_kinds_dims(f2v, orc, dev, kind, d, precision):
     """One epoch per (kind, d): VEC and masked layouts, b not dividing n
     (short last batch), isolated vertices, every force model."""
@@ -499,6 +501,15 @@ def test_config4_shape_low_d(f2v, orc, dev):
         assert losses[0] == pytest.approx(lref, rel=LOSS_RTOL["fast"])
         assert [ctr.attractive_evals, ctr.repulsive_evals] == [g.num_edges(), n * 5]
         zref = zr
+    # the same shape at the reference's arithmetic (rows_lowd_exact): each pair's
+    # fp64 distance runs over the columns in the reference's own order, so the
+    # epoch is bit-identical to the oracle's
+    cfg_x = dataclasses.replace(cfg, precision="exact")
+    z, losses, _ = run_epochs(f2v, dev, g, z0, cfg_x, first=0, run=1)
+    zr, lref = oracle_epoch(orc, g.row_offsets, g.col_indices, z0, 256, 5, 0.02, 0, "tdist", 1,
+                            "philox")
+    assert np.array_equal(z, zr.astype(np.float32))
+    assert losses[0] == pytest.approx(lref, rel=LOSS_RTOL["exact"])
 
 
 def test_exact_partial_sizing_identical(f2v, orc):
