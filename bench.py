@@ -134,12 +134,13 @@ class ClockSampler:
                     N.nvmlClocksThrottleReasonHwThermalSlowdown,
                     N.nvmlClocksThrottleReasonSwThermalSlowdown,
                     N.nvmlClocksThrottleReasonSwPowerCap]
-            while not self.stop.is_set():
+            while True:  # at least one sample, however short the timed region
                 sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
                 r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                 self.samples.append([str(sm), str(mx)] +
                                     ["Active" if r & b else "Not Active" for b in bits])
-                self.stop.wait(0.002)
+                if self.stop.wait(0.002):
+                    break
             self.source = "nvml"
             return
         except Exception:
