@@ -186,6 +186,11 @@ __global__ void seq_sum_kernel(const double* __restrict__ v, uint64_t n, double*
   if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = seq_sum(v, n, 0.0);
 }
 
+__global__ void fill_kernel(double* v, uint64_t n, double x) {
+  const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = x;
+}
+
 __global__ void iota_kernel(uint32_t* v, uint64_t n) {
   const uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) v[i] = uint32_t(i);
@@ -550,9 +555,9 @@ static double lloyd_once(Ctx& c, KmeansWork& w, const float* z, uint64_t n, uint
     return mix64(rng);
   };
   {  // k-means++ seeding, queued without a host round trip
-    std::vector<double> inf(n, std::numeric_limits<double>::infinity());
-    F2V_CUDA(cudaMemcpyAsync(dist2, inf.data(), sizeof(double) * n, cudaMemcpyHostToDevice,
-                             c.stream));
+    fill_kernel<<<grid_for(n), kTB, 0, c.stream>>>(dist2, n,
+                                                   std::numeric_limits<double>::infinity());
+    F2V_LAUNCHED(c.stream, "fill_kernel");
     seed_pick_kernel<<<1, kTB, 0, c.stream>>>(z, n, d, dist2, next(), 1, cen);
     F2V_LAUNCHED(c.stream, "seed_pick_kernel");
     ++c.launches;
@@ -564,7 +569,6 @@ static double lloyd_once(Ctx& c, KmeansWork& w, const float* z, uint64_t n, uint
       F2V_LAUNCHED(c.stream, "seed_pick_kernel");
       c.launches += 2;
     }
-    F2V_CUDA(cudaStreamSynchronize(c.stream));  // `inf` is pageable: the copy must be done
   }
   F2V_CUDA(cudaMemsetAsync(assign, 0xff, sizeof(int32_t) * n, c.stream));  // -1
   double inertia = std::numeric_limits<double>::infinity();

@@ -969,15 +969,22 @@ __device__ __forceinline__ void rows_exact128(const ForceParams& fp, uint32_t pa
   const uint32_t pkc = __shfl_sync(kFull, packed, min(lane, cnt - 1));
   const char* mine = reinterpret_cast<const char*>(((pkc & kNewBit) ? znew : zold) +
                                                    size_t(pkc & ~kNewBit) * d);
-  auto issue = [&](int k0, int st) {
+#if F2V_EXACT_LOAD != 2
+  // blocks are issued strictly in order: the pointers rotate by 8 lanes per
+  // block, so row i of the block being issued always sits in lane i (shuffles
+  // with constant lanes, no per-row index arithmetic)
+  unsigned long long rot = reinterpret_cast<unsigned long long>(mine);
+  const int rot_src = (lane + 8) & 31;
+  auto issue = [&](int, int st) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const char* src = reinterpret_cast<const char*>(
-          __shfl_sync(kFull, reinterpret_cast<unsigned long long>(mine), (k0 + i) & 31));
+      const char* src = reinterpret_cast<const char*>(__shfl_sync(kFull, rot, i));
       cp_async16(slots + (st * 8 + i) * kRowBytes, src + 16 * lane);
     }
     cp_async_commit();
+    rot = __shfl_sync(kFull, rot, rot_src);
   };
+#endif
   const int nblk = (cnt + 7) >> 3;
 #if F2V_EXACT_LOAD != 2
 #pragma unroll
