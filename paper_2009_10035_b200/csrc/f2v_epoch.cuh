@@ -283,6 +283,7 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
   const uint32_t p = item.p, u = item.u, cb = item.cb, c = item.c, nch = item.nch;
   DCHECK(p < a.n && u < a.n, "E p=%u u=%u n=%u", p, u, a.n);
   const uint32_t j = __ldg(a.state + u) >> 1;
+  const uint32_t needs_w = __ldg(a.needs + u);  // static during the launch; used at the end
   const uint32_t cs = cb + c;
   const uint32_t ps = __ldg(a.pslot + p);  // partial slots of u (used when nch > 1 or needs-L)
   DCHECK(c < nch && cs < a.chunks, "E c=%u nch=%u cs=%u chunks=%llu", c, nch, cs,
@@ -347,7 +348,7 @@ __device__ void do_E(const EpochArgs& a, const EItem& item, int lane, uint32_t* 
     q.push(a, lane, use, pk, zu, acc, lsum);
   }
   q.flush(a, lane, zu, acc, lsum);
-  const bool needs = a.needs[u] != 0;
+  const bool needs = needs_w != 0;
   if (nch == 1) {
     if (!needs) {
       do_negatives<KIND, K, VEC, MON, FAST, EMUL>(a, zn, j, neg_set(a, u, j), lane, zu, acc, lsum);

@@ -1,7 +1,6 @@
-python -m pytest tests/test_gpu_parity.py tests/test_gpu_shards.py tests/test_gpu_walk.py -x -q > gpurun_out/t_v34.log 2>&1; tail -3 gpurun_out/t_v34.log
 for r in 1 2; do for lib in default paper_2009_10035_b200/lib/libf2v_b200_base.so; do
   if [ "$lib" = default ]; then unset F2V_LIB; else export F2V_LIB=$PWD/$lib; fi
-  for c in c3 c2 c4; do
+  for c in c3 c2; do
   timeout 300 python bench.py --config $c --precision exact --steps 5 --warmup 3 --no-cpu-baseline --no-per-step 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$lib $c exact', round(d['ms_per_step'],3), round(d['roofline']['kernel_ms_per_launch'],3), 'fast', round(d['fast']['ms_per_step'],3), round(d['fast']['roofline']['kernel_ms_per_launch'],3))"
   done
-done; done > gpurun_out/ab_v34.log 2>&1; cat gpurun_out/ab_v34.log
+done; done > gpurun_out/ab_v35.log 2>&1; cat gpurun_out/ab_v35.log
