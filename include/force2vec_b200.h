@@ -281,6 +281,15 @@ int32_t f2v_read_embedding(const char* path, float** z_out, uint32_t* n_out, uin
  * first_label nullable, -1 = unlabeled */
 int32_t f2v_write_layout_tsv(const char* path, const float* z, uint32_t n, uint32_t d,
                              const int32_t* first_label);
+/* write_layout_svg (embedding_io.cpp:126-159): an 800 x 800 scatter, one circle per
+ * vertex coloured by its first label (12-colour palette); byte-identical output */
+int32_t f2v_write_layout_svg(const char* path, const float* z, uint32_t n, uint32_t d,
+                             const int32_t* first_label);
+/* load_labels (evaluation.cpp:175-199): "vertex_id label_id" lines, '#'/'%' comments,
+ * repeated vertices = multi-label.  Labels as a CSR over vertices, sorted and unique
+ * per vertex: *offsets_out u64[n + 1], *ids_out (both f2v_free) */
+int32_t f2v_load_labels(const char* path, uint32_t n, uint64_t** offsets_out, int32_t** ids_out,
+                        int32_t* num_classes_out, int32_t* multi_label_out);
 
 /* Evaluation (evaluation.cpp) on the device, over the context's graph and its
  * current embedding.  rng_state is the state word of the reference's Rng

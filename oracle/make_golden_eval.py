@@ -48,6 +48,19 @@ def io_cases():
     }
 
 
+def label_cases():
+    return {
+        "single": b"0 2\n1 0\n# comment\n2 1\n\n5 2\r\n",
+        "multi": b"% c\n0 1\n0 3\n2 0\n0 1\n4 7\n   \n",
+        "bad_token": b"0 1\nx 2\n",
+        "missing_label": b"0 1\n3\n",
+        "out_of_range": b"0 1\n9 2\n",
+        "lead_space": b" 1 2\n",
+        "junk_after": b"1 2abc\n3   4 5\n",
+        "empty": b"",
+    }
+
+
 def main():
     rs = np.random.default_rng(20260921)
     g = {}
@@ -68,6 +81,19 @@ def main():
         assert rev.write_layout_tsv(p, z2, lab) == 0
         g["io_tsv"] = np.frombuffer(open(p, "rb").read(), np.uint8)
         g["io_tsv_labels"] = lab
+        assert rev.write_layout_svg(p, z2, lab) == 0
+        g["io_svg"] = np.frombuffer(open(p, "rb").read(), np.uint8)
+        assert rev.write_layout_svg(p, z2) == 0
+        g["io_svg_nolabels"] = np.frombuffer(open(p, "rb").read(), np.uint8)
+        # label files (evaluation.cpp:175-199)
+        for name, content in label_cases().items():
+            open(p, "wb").write(content)
+            rc, off, ids, nc, multi, msg = rev.load_labels(p, 6)
+            g[f"lab_{name}_rc"] = np.int32(rc)
+            g[f"lab_{name}_msg"] = np.array(msg)
+            if rc == 0:
+                g[f"lab_{name}_off"], g[f"lab_{name}_ids"] = off, ids
+                g[f"lab_{name}_meta"] = np.array([nc, int(multi)], np.int32)
         names, rcs, msgs, outs = [], [], [], []
         for name, content in io_cases().items():
             open(p, "wb").write(content)

@@ -30,6 +30,10 @@ def lib():
                                              C.POINTER(C.c_uint32)])
         s(L, "ref_write_layout_tsv", C.c_int, [C.c_char_p, f32p, C.c_uint32, C.c_uint32,
                                                C.c_void_p])
+        s(L, "ref_write_layout_svg", C.c_int, [C.c_char_p, f32p, C.c_uint32, C.c_uint32,
+                                               C.c_void_p])
+        s(L, "ref_load_labels", C.c_int, [C.c_char_p, C.c_uint32, u64p, i32p,
+                                          C.POINTER(C.c_int), C.POINTER(C.c_int)])
         s(L, "ref_kmeans", C.c_int, [f32p, C.c_uint32, C.c_uint32, C.c_int,
                                      C.POINTER(C.c_uint64), C.c_int, C.c_int, i32p,
                                      C.POINTER(C.c_double)])
@@ -89,6 +93,24 @@ def write_layout_tsv(path, z, first_label=None):
     fl = None if first_label is None else np.ascontiguousarray(first_label, np.int32)
     return lib().ref_write_layout_tsv(str(path).encode(), z, z.shape[0], z.shape[1],
                                       None if fl is None else fl.ctypes.data_as(C.c_void_p))
+
+
+def write_layout_svg(path, z, first_label=None):
+    z = np.ascontiguousarray(z, np.float32)
+    fl = None if first_label is None else np.ascontiguousarray(first_label, np.int32)
+    return lib().ref_write_layout_svg(str(path).encode(), z, z.shape[0], z.shape[1],
+                                      None if fl is None else fl.ctypes.data_as(C.c_void_p))
+
+
+def load_labels(path, n, max_lines=100000):
+    """(rc, offsets, ids, num_classes, multi_label, message)"""
+    off = np.zeros(n + 1, np.uint64)
+    ids = np.zeros(max_lines, np.int32)
+    nc, multi = C.c_int(), C.c_int()
+    rc = lib().ref_load_labels(str(path).encode(), n, off, ids, C.byref(nc), C.byref(multi))
+    if rc:
+        return rc, None, None, 0, False, err()
+    return 0, off, ids[:int(off[-1])], nc.value, bool(multi.value), ""
 
 
 def kmeans(z, k, state, restarts=10, max_iters=300):

@@ -125,6 +125,39 @@ int ref_write_layout_tsv(const char* path, const float* z, std::uint32_t n, std:
   } catch (const std::exception& e) { return classify(e); }
 }
 
+int ref_write_layout_svg(const char* path, const float* z, std::uint32_t n, std::uint32_t d,
+                         const std::int32_t* first_label) {
+  try {
+    std::ofstream out(path, std::ios::binary);
+    LabeledNodes l;
+    if (first_label) {
+      l.labels.resize(n);
+      for (std::uint32_t u = 0; u < n; ++u)
+        if (first_label[u] >= 0) l.labels[u].push_back(first_label[u]);
+    }
+    write_layout_svg(out, to_matrix(z, n, d), first_label ? &l : nullptr);
+    return 0;
+  } catch (const std::exception& e) { return classify(e); }
+}
+
+// load_labels: CSR over vertices into caller buffers (ids sized >= the line count)
+int ref_load_labels(const char* path, std::uint32_t n, std::uint64_t* off, std::int32_t* ids,
+                    int* num_classes, int* multi) {
+  try {
+    std::ifstream in(path, std::ios::binary);
+    const LabeledNodes l = load_labels(in, n);
+    off[0] = 0;
+    std::uint64_t k = 0;
+    for (std::uint32_t u = 0; u < n; ++u) {
+      for (int c : l.labels[u]) ids[k++] = c;
+      off[u + 1] = k;
+    }
+    *num_classes = l.num_classes;
+    *multi = l.multi_label ? 1 : 0;
+    return 0;
+  } catch (const std::exception& e) { return classify(e); }
+}
+
 // ---- evaluation.cpp: clustering -------------------------------------------
 int ref_kmeans(const float* z, std::uint32_t n, std::uint32_t d, int k, std::uint64_t* state,
                int restarts, int max_iters, std::int32_t* assign_out, double* inertia_out) {

@@ -176,6 +176,10 @@ SYMBOLS = {
     "f2v_read_embedding": (_i32, [C.c_char_p, C.POINTER(C.POINTER(C.c_float)),
                                   C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "f2v_write_layout_tsv": (_i32, [C.c_char_p, _f32p, C.c_uint32, C.c_uint32, _vp]),
+    "f2v_write_layout_svg": (_i32, [C.c_char_p, _f32p, C.c_uint32, C.c_uint32, _vp]),
+    "f2v_load_labels": (_i32, [C.c_char_p, C.c_uint32, C.POINTER(C.POINTER(C.c_uint64)),
+                               C.POINTER(C.POINTER(C.c_int32)), C.POINTER(_i32),
+                               C.POINTER(_i32)]),
     "f2v_rng_state": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "f2v_kmeans": (_i32, [_vp, _i32, C.POINTER(C.c_uint64), _i32, _i32, _i32p,
                           C.POINTER(C.c_double)]),

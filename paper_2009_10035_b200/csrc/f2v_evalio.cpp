@@ -197,6 +197,99 @@ void write_layout_tsv(const char* path, const float* z, uint32_t n, uint32_t d,
   if (!ok || std::fflush(fp.f) != 0) fail(F2V_EIO, "failed writing layout tsv");
 }
 
+// write_layout_svg (embedding_io.cpp:126-159).  The reference streams its doubles
+// with the default ostream format (%g, 6 significant digits); the coordinates
+// are float arithmetic widened at the end, as in the reference's expressions.
+void write_layout_svg(const char* path, const float* z, uint32_t n, uint32_t d,
+                      const int32_t* first_label) {
+  if (d != 2) fail(F2V_EUSAGE, "layout export requires a 2-D embedding (train with dim 2)");
+  File fp(path, "wb");
+  if (!fp.f) fail(F2V_EIO, std::string("cannot open ") + path + " for writing");
+  float min_x = INFINITY, max_x = -INFINITY, min_y = INFINITY, max_y = -INFINITY;
+  for (uint32_t u = 0; u < n; ++u) {
+    min_x = std::min(min_x, z[size_t(u) * 2]);
+    max_x = std::max(max_x, z[size_t(u) * 2]);
+    min_y = std::min(min_y, z[size_t(u) * 2 + 1]);
+    max_y = std::max(max_y, z[size_t(u) * 2 + 1]);
+  }
+  const float span_x = std::max(max_x - min_x, 1e-9f);
+  const float span_y = std::max(max_y - min_y, 1e-9f);
+  const int size = 800, margin = 20;
+  static const char* kPalette[12] = {"#1f77b4", "#ff7f0e", "#2ca02c", "#d62728", "#9467bd",
+                                     "#8c564b", "#e377c2", "#7f7f7f", "#bcbd22", "#17becf",
+                                     "#aec7e8", "#ffbb78"};
+  std::string buf = "<svg xmlns=\"http://www.w3.org/2000/svg\" width=\"800\" height=\"800\" "
+                    "viewBox=\"0 0 800 800\">\n";
+  bool ok = true;
+  char num[64];
+  for (uint32_t u = 0; u < n; ++u) {
+    const double x = margin + (z[size_t(u) * 2] - min_x) / span_x * (size - 2 * margin);
+    const double y = margin + (max_y - z[size_t(u) * 2 + 1]) / span_y * (size - 2 * margin);
+    const char* color = kPalette[0];
+    if (first_label && first_label[u] >= 0) color = kPalette[first_label[u] % 12];
+    buf += "<circle cx=\"";
+    std::snprintf(num, sizeof(num), "%g", x);
+    buf += num;
+    buf += "\" cy=\"";
+    std::snprintf(num, sizeof(num), "%g", y);
+    buf += num;
+    buf += "\" r=\"2.5\" fill=\"";
+    buf += color;
+    buf += "\" fill-opacity=\"0.8\"/>\n";
+    if (buf.size() > (1u << 20)) {
+      ok = ok && std::fwrite(buf.data(), 1, buf.size(), fp.f) == buf.size();
+      buf.clear();
+    }
+  }
+  buf += "</svg>\n";
+  ok = ok && std::fwrite(buf.data(), 1, buf.size(), fp.f) == buf.size();
+  if (!ok || std::fflush(fp.f) != 0) fail(F2V_EIO, "failed writing layout svg");
+}
+
+// load_labels (evaluation.cpp:175-199)
+void load_labels(const char* path, uint32_t n, std::vector<uint64_t>& off, std::vector<int32_t>& ids,
+                 int32_t& num_classes, int32_t& multi) {
+  const std::vector<char> buf = slurp(path);
+  std::vector<std::vector<int32_t>> labels(n);
+  const char* cur = buf.data();
+  const char* const eof = buf.data() + buf.size();
+  uint64_t line_no = 0;
+  int max_label = -1;
+  while (cur != eof) {
+    const char* nl = static_cast<const char*>(std::memchr(cur, '\n', size_t(eof - cur)));
+    const char* p = cur;
+    const char* end = nl ? nl : eof;
+    cur = nl ? nl + 1 : eof;
+    ++line_no;
+    if (end > p && end[-1] == '\r') --end;
+    const char* q = p;
+    while (q < end && is_space(*q)) ++q;
+    if (q == end || *p == '#' || *p == '%') continue;
+    uint64_t u = 0, label = 0;
+    const auto r1 = std::from_chars(p, end, u);
+    p = r1.ptr;
+    while (p < end && is_space(*p)) ++p;
+    const auto r2 = std::from_chars(p, end, label);
+    if (r1.ec != std::errc() || r2.ec != std::errc())
+      fail(F2V_ERANGE, "bad label line " + std::to_string(line_no));
+    if (u >= n) fail(F2V_ERANGE, "label vertex id out of range at line " + std::to_string(line_no));
+    labels[u].push_back(int32_t(label));
+    max_label = std::max(max_label, int(label));
+  }
+  num_classes = max_label + 1;
+  multi = 0;
+  off.assign(size_t(n) + 1, 0);
+  ids.clear();
+  for (uint32_t u = 0; u < n; ++u) {
+    auto& ls = labels[u];
+    std::sort(ls.begin(), ls.end());
+    ls.erase(std::unique(ls.begin(), ls.end()), ls.end());
+    if (ls.size() > 1) multi = 1;
+    ids.insert(ids.end(), ls.begin(), ls.end());
+    off[u + 1] = ids.size();
+  }
+}
+
 // ------------------------------------------------------ link-prediction data
 bool has_arc(const uint64_t* rowptr, const uint32_t* col, uint32_t u, uint32_t v) {
   return std::binary_search(col + rowptr[u], col + rowptr[u + 1], v);
@@ -390,6 +483,30 @@ int32_t f2v_read_embedding(const char* path, float** z_out, uint32_t* n_out, uin
 int32_t f2v_write_layout_tsv(const char* path, const float* z, uint32_t n, uint32_t d,
                              const int32_t* first_label) {
   return guard(nullptr, [&] { write_layout_tsv(path, z, n, d, first_label); });
+}
+
+int32_t f2v_write_layout_svg(const char* path, const float* z, uint32_t n, uint32_t d,
+                             const int32_t* first_label) {
+  return guard(nullptr, [&] { write_layout_svg(path, z, n, d, first_label); });
+}
+
+int32_t f2v_load_labels(const char* path, uint32_t n, uint64_t** offsets_out, int32_t** ids_out,
+                        int32_t* num_classes_out, int32_t* multi_label_out) {
+  return guard(nullptr, [&] {
+    std::vector<uint64_t> off;
+    std::vector<int32_t> ids;
+    int32_t nc = 0, multi = 0;
+    load_labels(path, n, off, ids, nc, multi);
+    uint64_t* o = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * off.size()));
+    int32_t* i = static_cast<int32_t*>(std::malloc(sizeof(int32_t) * std::max<size_t>(1, ids.size())));
+    if (!o || !i) throw std::bad_alloc();
+    std::memcpy(o, off.data(), sizeof(uint64_t) * off.size());
+    if (!ids.empty()) std::memcpy(i, ids.data(), sizeof(int32_t) * ids.size());
+    *offsets_out = o;
+    *ids_out = i;
+    *num_classes_out = nc;
+    *multi_label_out = multi;
+  });
 }
 
 uint64_t f2v_rng_state(uint64_t seed, uint64_t stream) { return rng_init(seed, stream); }

@@ -21,6 +21,7 @@ embedding being evaluated.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -77,8 +78,7 @@ def read_embedding(path: str) -> np.ndarray:
         _lib.f2v_free(ptr)
 
 
-def write_layout_tsv(path: str, z: np.ndarray, labels: Optional["LabeledNodes"] = None) -> None:
-    """``write_layout_tsv`` (embedding_io.cpp:102-124): "id<TAB>x<TAB>y[<TAB>label]"."""
+def _layout(fn, path, z, labels):
     z = np.ascontiguousarray(z, np.float32)
     first = None
     if labels is not None:
@@ -86,9 +86,19 @@ def write_layout_tsv(path: str, z: np.ndarray, labels: Optional["LabeledNodes"] 
         for u, ls in enumerate(labels.labels[:z.shape[0]]):
             if len(ls):
                 first[u] = ls[0]
-    _ck_global(_lib.f2v_write_layout_tsv(
-        str(path).encode(), z, z.shape[0], z.shape[1] if z.ndim == 2 else 0,
-        first.ctypes.data_as(C.c_void_p) if first is not None else None))
+    _ck_global(fn(str(path).encode(), z, z.shape[0], z.shape[1] if z.ndim == 2 else 0,
+                  first.ctypes.data_as(C.c_void_p) if first is not None else None))
+
+
+def write_layout_tsv(path: str, z: np.ndarray, labels: Optional["LabeledNodes"] = None) -> None:
+    """``write_layout_tsv`` (embedding_io.cpp:102-124): "id<TAB>x<TAB>y[<TAB>label]"."""
+    _layout(_lib.f2v_write_layout_tsv, path, z, labels)
+
+
+def write_layout_svg(path: str, z: np.ndarray, labels: Optional["LabeledNodes"] = None) -> None:
+    """``write_layout_svg`` (embedding_io.cpp:126-159): an 800 x 800 scatter of a
+    2-D embedding, points coloured by their first label."""
+    _layout(_lib.f2v_write_layout_svg, path, z, labels)
 
 
 # ----------------------------------------------------------------- clustering
@@ -240,11 +250,23 @@ class LabeledNodes:  # evaluation.hpp:73-77
 def load_labels(path_or_lines, n: int) -> LabeledNodes:
     """``load_labels`` (evaluation.cpp:175-199): "vertex_id label_id" lines,
     '#' / '%' comments, repeated vertices = multi-label."""
-    if isinstance(path_or_lines, (str, bytes)):
-        with open(path_or_lines, "r") as f:
-            lines = f.read().split("\n")
-    else:
-        lines = list(path_or_lines)
+    if isinstance(path_or_lines, (str, bytes, os.PathLike)):  # the library's parser
+        off, ids = C.POINTER(C.c_uint64)(), C.POINTER(C.c_int32)()
+        nc, multi = C.c_int32(), C.c_int32()
+        rc = _lib.f2v_load_labels(os.fsencode(path_or_lines), n, C.byref(off), C.byref(ids),
+                                  C.byref(nc), C.byref(multi))
+        # code 3 carries both FormatError ("bad label line N") and RangeError
+        _raise(rc, _lib.f2v_global_error(),
+               format_errors=(_lib.f2v_global_error() or b"").startswith(b"bad label line"))
+        try:
+            o = np.ctypeslib.as_array(off, shape=(n + 1,)).copy()
+            i = np.ctypeslib.as_array(ids, shape=(max(int(o[-1]), 1),)).copy()
+        finally:
+            _lib.f2v_free(off)
+            _lib.f2v_free(ids)
+        return LabeledNodes([[int(c) for c in i[int(o[u]):int(o[u + 1])]] for u in range(n)],
+                            nc.value, bool(multi.value))
+    lines = list(path_or_lines)
     out = LabeledNodes(labels=[[] for _ in range(n)])
     max_label = -1
     for no, line in enumerate(lines, 1):

@@ -86,6 +86,36 @@ def test_layout_tsv_bytes_equal_reference(tmp_path):
         ev.write_layout_tsv(p, G["io_z"])
 
 
+def test_layout_svg_bytes_equal_reference(tmp_path):
+    p = tmp_path / "l.svg"
+    lab = ev.LabeledNodes(labels=[[int(x)] if x >= 0 else [] for x in G["io_tsv_labels"]])
+    z2 = G["io_z"][:, :2].copy()
+    ev.write_layout_svg(p, z2, lab)
+    assert p.read_bytes() == G["io_svg"].tobytes()
+    ev.write_layout_svg(p, z2)
+    assert p.read_bytes() == G["io_svg_nolabels"].tobytes()
+    with pytest.raises(f2v.UsageError, match="2-D embedding"):
+        ev.write_layout_svg(p, G["io_z"])
+
+
+def test_load_labels_file_cases_match_reference(tmp_path):
+    from make_golden_eval import label_cases
+    for name, content in label_cases().items():
+        p = tmp_path / f"{name}.txt"
+        p.write_bytes(content)
+        rc, msg = int(G[f"lab_{name}_rc"]), str(G[f"lab_{name}_msg"])
+        if rc == 0:
+            lab = ev.load_labels(str(p), 6)
+            off, ids = G[f"lab_{name}_off"], G[f"lab_{name}_ids"]
+            want = [[int(c) for c in ids[int(off[u]):int(off[u + 1])]] for u in range(6)]
+            assert lab.labels == want, name
+            assert [lab.num_classes, int(lab.multi_label)] == list(G[f"lab_{name}_meta"]), name
+        else:
+            with pytest.raises(f2v.Error) as e:
+                ev.load_labels(str(p), 6)
+            assert str(e.value) == msg, name
+
+
 @pytest.mark.parametrize("tag", ["link", "linkd"])
 def test_build_link_dataset_equals_reference(tag):
     rowptr = G["mod_rowptr"] if tag == "link" else G["linkd_rowptr"]

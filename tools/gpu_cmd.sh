@@ -1,8 +1,6 @@
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_v9.log 2>&1; tail -1 gpurun_out/smoke_v9.log
-python -m pytest tests -m gpu -x -q > gpurun_out/r2_gputests_v9.log 2>&1; tail -3 gpurun_out/r2_gputests_v9.log
-python bench.py > gpurun_out/r2_bench_default_v9.json 2> gpurun_out/r2_bench_default_v9.err; tail -c 200 gpurun_out/r2_bench_default_v9.json
-python bench.py --impl reference > gpurun_out/r2_bench_reference_v9.json 2> gpurun_out/r2_bench_reference_v9.err
-for c in c1 c2 c4; do python bench.py --config $c --no-cpu-baseline > gpurun_out/r2_bench_${c}_v9.json 2> gpurun_out/r2_bench_${c}_v9.err; done
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/r2_c3_launches_v9.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-fast --no-per-step > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:epoch_kernel --launch-skip 5 --launch-count 1 -o gpurun_out/r2_c3_fast_v9 python bench.py --precision fast --steps 1 --warmup 3 --no-cpu-baseline --no-per-step > /dev/null 2>&1
-ls gpurun_out | grep v9
+for r in 1 2; do for lib in default paper_2009_10035_b200/lib/libf2v_b200_p64.so paper_2009_10035_b200/lib/libf2v_b200_p128.so paper_2009_10035_b200/lib/libf2v_b200_p512.so; do
+  if [ "$lib" = default ]; then unset F2V_LIB; else export F2V_LIB=$PWD/$lib; fi
+  for c in c2 c3; do
+  timeout 300 python bench.py --config $c --precision exact --steps 5 --warmup 3 --no-cpu-baseline --no-per-step 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$lib $c exact', round(d['ms_per_step'],3), round(d['roofline']['kernel_ms_per_launch'],3), 'fast', round(d['fast']['ms_per_step'],3), round(d['fast']['roofline']['kernel_ms_per_launch'],3))"
+  done
+done; done > gpurun_out/ab_v37.log 2>&1; cat gpurun_out/ab_v37.log
